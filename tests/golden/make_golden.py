@@ -1,0 +1,251 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container only (needs /root/reference, read-only):
+
+    python tests/golden/make_golden.py
+
+It imports `binfec` from /root/reference/pkg/src and writes
+tests/golden/golden_r8.npz (full arrays, small) and tests/golden/golden_r16.json
+(sha256 digests + sampled entries of the large r=16 arrays).  The committed
+outputs pin the oracle (tests/test_oracle_golden.py) and, through it, the GPU
+path.  Nothing on the GPU box reads /root/reference.
+
+Inputs are drawn from a pure-Python restatement of the counter-based generator
+(identical to oracle/lch_oracle.c `orc_key` and csrc/lch_gen.cu),
+so tests can regenerate them without storing the r=16 payloads.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import random
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from binfec import batch as ref_batch  # noqa: E402
+from binfec import rs as ref_rs  # noqa: E402
+from binfec import walsh as ref_walsh  # noqa: E402
+from binfec.basis import build_basis_tables  # noqa: E402
+from binfec.derivative import derivative_fast  # noqa: E402
+from binfec.field import tables_for  # noqa: E402
+from binfec.transform import CoeffVec, EvalVec, forward, inverse  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+M64 = (1 << 64) - 1
+GAMMA = 0x9E3779B97F4A7C15
+
+
+def mix64(z: int) -> int:
+    z &= M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def key(seed: int, cw: int, pos: int) -> int:
+    s = mix64(seed + GAMMA)
+    return mix64(s + (((cw << 32) | pos) * GAMMA))
+
+
+def gen_symbols(seed: int, r: int, cw: int, length: int) -> list[int]:
+    mask = (1 << r) - 1
+    return [key(seed, cw, j) & mask for j in range(length)]
+
+
+def gen_erasures(seed: int, n: int, count: int, cw: int) -> list[int]:
+    order = sorted(range(n), key=lambda j: (key(seed, cw, j) >> 1, j))
+    return sorted(order[:count])
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.asarray(a, dtype="<u4" if np.asarray(a).dtype == np.uint32 else "<u2").tobytes()).hexdigest()
+
+
+def sample(a, n=64, seed=7) -> dict:
+    a = np.asarray(a)
+    rng = random.Random(seed)
+    idx = sorted(rng.sample(range(a.size), min(n, a.size)))
+    return {"idx": idx, "val": [int(a.flat[i]) for i in idx]}
+
+
+def tables_of(ft, bt) -> dict:
+    return dict(
+        log=np.asarray(ft.log, np.uint16), exp=np.asarray(ft.exp, np.uint16),
+        w_hat=np.asarray([x for lvl in bt.w_hat for x in lvl], np.uint16),
+        w_prime=np.asarray(bt.w_prime, np.uint16),
+        b_prod=np.asarray(bt.b_prod, np.uint16),
+        b_prod_inv=np.asarray(bt.b_prod_inv, np.uint16),
+        fwht_log=np.asarray(ref_walsh._fwht_of_log(ft), np.uint32),
+        w_on_basis=np.asarray(bt.w_on_basis, np.uint16),
+        w_norm=np.asarray(bt.w_norm, np.uint16))
+
+
+def make_r8() -> None:
+    ft = tables_for(8)
+    bt = build_basis_tables(ft, 256)
+    out = {f"tab_{k}": v for k, v in tables_of(ft, bt).items()}
+
+    # transforms: every size, shifts {0, h, random}, forward + inverse + derivative
+    rng = random.Random(1404)
+    cases = []
+    for lg in range(0, 9):
+        h = 1 << lg
+        for shift in sorted({0, h % 256, rng.randrange(256), 255}):
+            d = [rng.randrange(256) for _ in range(h)]
+            cases.append((h, shift, d))
+    fw, inv, der, meta = [], [], [], []
+    for h, shift, d in cases:
+        fw.append(forward(bt, CoeffVec(d), shift).data)
+        inv.append(inverse(bt, EvalVec(d, shift)).data)
+        der.append(derivative_fast(bt, CoeffVec(d)).data)
+        meta.append((h, shift))
+    flat = lambda xs: np.asarray([x for v in xs for x in v], np.uint16)  # noqa: E731
+    out["tr_meta"] = np.asarray(meta, np.int64)
+    out["tr_in"] = flat([d for _, _, d in cases])
+    out["tr_fwd"] = flat(fw)
+    out["tr_inv"] = flat(inv)
+    out["tr_der"] = flat(der)
+
+    # fwht + locator logs for several patterns (walsh.py)
+    pats = []
+    for size in (1, 2, 40, 128, 200, 255):
+        pats.append(sorted(random.Random(size).sample(range(256), size)))
+    out["loc_mask"] = np.zeros((len(pats), 256), np.uint8)
+    out["loc_val"] = np.zeros((len(pats), 256), np.uint16)
+    for t, p in enumerate(pats):
+        out["loc_mask"][t, p] = 1
+        lv = ref_walsh.locator_values(ft, p)
+        for j, v in lv.pi_bar.items():
+            out["loc_val"][t, j] = v
+        for j, v in lv.pi_prime.items():
+            out["loc_val"][t, j] = v
+
+    # config 1: (256, 128), 64 codewords, 128 per-codeword erasures (seed ...801)
+    seed_m, seed_e = 1404345801, 1404345801 ^ 0xE
+    cp = ref_rs.CodeParams(8, 128)
+    msgs, cws, masks, decs, junk_out = [], [], [], [], []
+    for cw in range(64):
+        m = gen_symbols(seed_m, 8, cw, 128)
+        c = ref_rs.encode(cp, bt, m).symbols
+        e = gen_erasures(seed_e, 256, 128, cw)
+        rx = [0 if j in set(e) else s for j, s in enumerate(c)]
+        dec = ref_rs.decode(cp, bt, ft, rx, ref_rs.ErasurePattern.of(256, e))
+        assert dec == m
+        # non-codeword input: the decoder's output is then a deterministic
+        # function of every intermediate step (locator, phi, transforms, derivative)
+        junk = gen_symbols(seed_m ^ 0x5A5A, 8, cw, 256)
+        jd = ref_rs.decode(cp, bt, ft, junk, ref_rs.ErasurePattern.of(256, e))
+        msgs.append(m); cws.append(c); decs.append(dec); junk_out.append(jd)
+        mk = np.zeros(256, np.uint8); mk[e] = 1; masks.append(mk)
+    out["cfg1_msg"] = np.asarray(msgs, np.uint16)
+    out["cfg1_cw"] = np.asarray(cws, np.uint16)
+    out["cfg1_mask"] = np.asarray(masks, np.uint8)
+    out["cfg1_junk_dec"] = np.asarray(junk_out, np.uint16)
+
+    # every power-of-two k (rs.py), one codeword each, through BatchCodec too
+    for k in (1, 2, 4, 16, 64, 256):
+        cpk = ref_rs.CodeParams(8, k)
+        m = np.asarray([gen_symbols(77, 8, cw, k) for cw in range(5)], np.uint16)
+        enc = ref_batch.BatchCodec(cpk, bt).encode(m)
+        for row in range(5):
+            assert list(enc[row]) == ref_rs.encode(cpk, bt, [int(x) for x in m[row]]).symbols
+        out[f"k{k}_msg"] = m
+        out[f"k{k}_cw"] = enc
+    np.savez_compressed(os.path.join(HERE, "golden_r8.npz"), **out)
+
+
+def make_r16() -> None:
+    ft = tables_for(16)
+    bt = build_basis_tables(ft, 1 << 16)
+    res: dict = {"tables": {}}
+    for k, v in tables_of(ft, bt).items():
+        res["tables"][k] = {"sha256": digest(v), "sample": sample(v), "size": int(v.size)}
+
+    # config 2: transforms at h = 2^16, two seeded polynomials, shift 0 and 12345
+    res["transform"] = []
+    for t, shift in enumerate((0, 12345)):
+        d = gen_symbols(1404345802, 16, t, 1 << 16)
+        fwd = forward(bt, CoeffVec(d), shift).data
+        inv = inverse(bt, EvalVec(d, shift)).data
+        der = derivative_fast(bt, CoeffVec(d)).data
+        res["transform"].append({
+            "seed": 1404345802, "cw": t, "h": 1 << 16, "shift": shift,
+            "fwd": {"sha256": digest(fwd), "sample": sample(fwd)},
+            "inv": {"sha256": digest(inv), "sample": sample(inv)},
+            "der": {"sha256": digest(der), "sample": sample(der)}})
+    # smaller sizes, full arrays (cheap): h = 2^10 at several shifts
+    res["transform_small"] = []
+    for shift in (0, 1024, 4096 * 3, 65535):
+        d = gen_symbols(99, 16, shift, 1024)
+        res["transform_small"].append({
+            "seed": 99, "cw": shift, "h": 1024, "shift": shift,
+            "fwd": forward(bt, CoeffVec(d), shift).data,
+            "inv": inverse(bt, EvalVec(d, shift)).data,
+            "der": derivative_fast(bt, CoeffVec(d)).data})
+
+    # config 3: encode, two codewords of RS(2^16, 2^15)
+    cp = ref_rs.CodeParams(16, 1 << 15)
+    res["encode"] = []
+    for cw in range(2):
+        m = gen_symbols(1404345803, 16, cw, 1 << 15)
+        c = ref_rs.encode(cp, bt, m).symbols
+        res["encode"].append({"seed": 1404345803, "cw": cw,
+                              "parity": {"sha256": digest(c[1 << 15:]), "sample": sample(c[1 << 15:])}})
+    # config 4: decode with 2^15 erasures; a true codeword and a non-codeword
+    seed_e = 1404345804
+    e = gen_erasures(seed_e, 1 << 16, 1 << 15, 0)
+    pat = ref_rs.ErasurePattern.of(1 << 16, e)
+    m = gen_symbols(1404345803, 16, 0, 1 << 15)
+    c = ref_rs.encode(cp, bt, m).symbols
+    es = set(e)
+    rx = [0 if j in es else s for j, s in enumerate(c)]
+    assert ref_rs.decode(cp, bt, ft, rx, pat) == m
+    junk = gen_symbols(1404345804 ^ 0x5A5A, 16, 0, 1 << 16)
+    jd = ref_rs.decode(cp, bt, ft, junk, pat)
+    lv = ref_walsh.locator_values(ft, e)
+    loc = np.zeros(1 << 16, np.uint16)
+    for j, v in lv.pi_bar.items():
+        loc[j] = v
+    for j, v in lv.pi_prime.items():
+        loc[j] = v
+    res["decode"] = {"erasure_seed": seed_e, "erasure_cw": 0, "count": 1 << 15,
+                     "pattern_sha256": digest(np.asarray(e, np.uint32)),
+                     "locator": {"sha256": digest(loc), "sample": sample(loc)},
+                     "junk_seed": 1404345804 ^ 0x5A5A,
+                     "junk_out": {"sha256": digest(jd), "sample": sample(jd)}}
+    # small locator pattern (walsh test_r16 style)
+    e100 = sorted(random.Random(54).sample(range(1 << 16), 100))
+    lv = ref_walsh.locator_values(ft, e100)
+    loc = np.zeros(1 << 16, np.uint16)
+    for j, v in lv.pi_bar.items():
+        loc[j] = v
+    for j, v in lv.pi_prime.items():
+        loc[j] = v
+    res["locator100"] = {"erased": e100, "sha256": digest(loc), "sample": sample(loc)}
+
+    # test_batch.py:57-67 analogue: (2^16, 256), 60,000 shared erasures, BatchCodec
+    cpb = ref_rs.CodeParams(16, 256)
+    codec = ref_batch.BatchCodec(cpb, bt)
+    msgs = np.asarray([gen_symbols(84, 16, cw, 256) for cw in range(3)], np.uint16)
+    enc = codec.encode(msgs)
+    e6 = gen_erasures(85, 1 << 16, 60000, 0)
+    junk = np.asarray([gen_symbols(86, 16, cw, 1 << 16) for cw in range(3)], np.uint16)
+    jd = codec.decode(junk, set(e6))
+    res["batch_k256"] = {"msg_seed": 84, "erasure_seed": 85, "count": 60000, "junk_seed": 86,
+                         "enc_sha256": digest(enc), "junk_dec_sha256": digest(jd),
+                         "junk_dec_sample": sample(jd)}
+    with open(os.path.join(HERE, "golden_r16.json"), "w") as fh:
+        json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    make_r8()
+    print("r8 done", flush=True)
+    make_r16()
+    print("r16 done", flush=True)

@@ -1,0 +1,606 @@
+// C ABI (include/lch.h): context, pass planner and the codec pipelines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/lch.h"
+#include "lch_kernels.h"
+#include "lch_tables.h"
+
+using namespace lch;
+
+struct lch_ctx {
+  Tables t;
+  int max_lg_h = 0;
+  bool dev_ready = false;
+  int device = -1;
+  uint16_t *d_w_hat = nullptr, *d_b_prod = nullptr, *d_b_prod_inv = nullptr;
+  uint16_t *d_exp = nullptr, *d_log = nullptr;
+  uint32_t *d_fwht_log = nullptr;
+  int64_t launches = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+#define LCH_TRY(expr)              \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != LCH_OK) return rc_; \
+  } while (0)
+
+int cu(cudaError_t e) { return e == cudaSuccess ? LCH_OK : (e == cudaErrorMemoryAllocation ? LCH_ENOMEM : LCH_ECUDA); }
+
+template <class T>
+int upload(T *&dst, const std::vector<T> &src) {
+  if (src.empty()) return LCH_OK;
+  LCH_TRY(cu(cudaMalloc(&dst, src.size() * sizeof(T))));
+  return cu(cudaMemcpy(dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+int ensure_device(lch_ctx *c) {
+  std::lock_guard<std::mutex> g(c->mu);
+  if (c->dev_ready) return LCH_OK;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return LCH_ECUDA;
+  }
+  LCH_TRY(cu(cudaGetDevice(&c->device)));
+  LCH_TRY(upload(c->d_w_hat, c->t.w_hat));
+  LCH_TRY(upload(c->d_b_prod, c->t.b_prod));
+  LCH_TRY(upload(c->d_b_prod_inv, c->t.b_prod_inv));
+  LCH_TRY(upload(c->d_exp, c->t.exp));
+  LCH_TRY(upload(c->d_log, c->t.log));
+  LCH_TRY(upload(c->d_fwht_log, c->t.fwht_log));
+  // keep freed scratch in the stream-ordered pool (no re-mapping per call)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  c->dev_ready = true;
+  return LCH_OK;
+}
+
+// Stream-ordered scratch allocation freed at scope exit.
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void *> ptrs;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch() {
+    for (void *p : ptrs) cudaFreeAsync(p, s);
+  }
+  template <class T>
+  int alloc(T *&p, size_t count) {
+    void *v = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMallocAsync(&v, count * sizeof(T), s);
+    if (e != cudaSuccess) return cu(e);
+    ptrs.push_back(v);
+    p = static_cast<T *>(v);
+    return LCH_OK;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// planner: group a sequence of per-level ops into tile passes of <= TPB_MAX
+// distinct position bits, in order.
+
+struct LOp {
+  int kind;
+  int level;
+  uint32_t hs;
+  const uint16_t *table;
+};
+
+struct Plan {
+  std::vector<LOp> ops;
+  std::vector<int> bits;  // sorted tile bits
+};
+
+bool low_bits_only(const std::vector<int> &bits, int tpb) {
+  for (int b : bits)
+    if (b >= tpb) return false;
+  return true;
+}
+
+std::vector<Plan> plan_passes(const std::vector<LOp> &ops, int lgH, bool raw_in, bool raw_out) {
+  const int tpb = std::min(TPB_MAX, lgH);
+  std::vector<Plan> out;
+  Plan cur;
+  auto has = [](const std::vector<int> &v, int b) { return std::find(v.begin(), v.end(), b) != v.end(); };
+  for (const LOp &op : ops) {
+    if (op.kind != OP_SCALE && !has(cur.bits, op.level)) {
+      if (int(cur.bits.size()) == tpb) {
+        out.push_back(cur);
+        cur = Plan();
+      }
+      cur.bits.push_back(op.level);
+    }
+    cur.ops.push_back(op);
+    if (int(cur.ops.size()) == MAXOPS) {
+      out.push_back(cur);
+      cur = Plan();
+    }
+  }
+  if (!cur.ops.empty() || out.empty()) out.push_back(cur);
+  if (raw_in && !low_bits_only(out.front().bits, tpb)) out.insert(out.begin(), Plan());
+  if (raw_out && !low_bits_only(out.back().bits, tpb)) out.push_back(Plan());
+  for (size_t i = 0; i < out.size(); ++i) {
+    Plan &p = out[i];
+    const bool raw = (i == 0 && raw_in) || (i + 1 == out.size() && raw_out);
+    if (raw) {
+      p.bits.clear();
+      for (int b = 0; b < tpb; ++b) p.bits.push_back(b);
+    } else {
+      for (int b = 0; int(p.bits.size()) < tpb && b < lgH; ++b)
+        if (!has(p.bits, b)) p.bits.push_back(b);
+    }
+    std::sort(p.bits.begin(), p.bits.end());
+  }
+  return out;
+}
+
+void fill_bits(const std::vector<int> &bits, int lgH, int *gbit, int &nnb, int *nbit) {
+  for (size_t m = 0; m < bits.size(); ++m) gbit[m] = bits[m];
+  nnb = 0;
+  for (int b = 0; b < lgH; ++b)
+    if (std::find(bits.begin(), bits.end(), b) == bits.end()) nbit[nnb++] = b;
+}
+
+RawIO make_raw(uint16_t *ptr, int64_t stride) {
+  RawIO io{};
+  io.ptr = ptr;
+  io.row_stride = stride;
+  io.vec = (reinterpret_cast<uintptr_t>(ptr) % 16 == 0) && (stride % 8 == 0);
+  return io;
+}
+
+template <int R, uint32_t POLY>
+int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, const RawIO *raw_in,
+             const uint4 *bs_in, const RawIO *raw_out, uint4 *work, cudaStream_t s) {
+  const int ngroups = int((batch + GROUP - 1) / GROUP);
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const Plan &pl = plan[i];
+    PassParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.nops = int(pl.ops.size());
+    for (int o = 0; o < p.nops; ++o) {
+      const LOp &op = pl.ops[o];
+      p.ops[o].kind = op.kind;
+      p.ops[o].level = op.level;
+      p.ops[o].hs = op.hs;
+      p.ops[o].table = op.table;
+      p.ops[o].m = 0;
+      if (op.kind != OP_SCALE)
+        p.ops[o].m = int(std::find(pl.bits.begin(), pl.bits.end(), op.level) - pl.bits.begin());
+    }
+    p.tpb = int(pl.bits.size());
+    p.lgH = lgH;
+    fill_bits(pl.bits, lgH, p.gbit, p.nnb, p.nbit);
+    p.batch = batch;
+    const bool first = i == 0, last = i + 1 == plan.size();
+    p.in_mode = (first && raw_in) ? IO_RAW : IO_BS;
+    p.out_mode = (last && raw_out) ? IO_RAW : IO_BS;
+    if (p.in_mode == IO_RAW) p.raw_in = *raw_in;
+    if (p.out_mode == IO_RAW) p.raw_out = *raw_out;
+    p.bs_in = (first && bs_in) ? bs_in : work;
+    p.bs_out = work;
+    p.w_hat = c->d_w_hat;
+    for (int l = 0; l <= c->t.levels && l < 17; ++l) p.w_hat_off[l] = c->t.w_hat_off[l];
+    LCH_TRY(cu(launch_pass<R, POLY>(p, ngroups, s)));
+    c->launches++;
+  }
+  return LCH_OK;
+}
+
+size_t bs_bytes(int R, int64_t batch, int lgH) {
+  const int64_t ngroups = (batch + GROUP - 1) / GROUP;
+  return size_t(ngroups) * (size_t(1) << lgH) * 32 * R * 4;
+}
+
+template <int R>
+int run_gather(lch_ctx *c, const uint4 *g, uint4 *t, int lgH_in, int lgH_out, int64_t batch,
+               cudaStream_t s) {
+  // The kernel sums over every tile bit, so each pass's tile is exactly one
+  // group of <= TPB_MAX consecutive bits; the groups partition [0, lgH_in).
+  const int ngroups = int((batch + GROUP - 1) / GROUP);
+  bool first = true;
+  for (int b0 = 0; b0 < lgH_in; b0 += TPB_MAX) {
+    GatherParams p;
+    std::memset(&p, 0, sizeof(p));
+    std::vector<int> bits;
+    for (int b = b0; b < std::min(b0 + TPB_MAX, lgH_in); ++b) bits.push_back(b);
+    p.tpb = int(bits.size());
+    p.lgH_in = lgH_in;
+    p.lgH_out = lgH_out;
+    fill_bits(bits, lgH_in, p.gbit, p.nnb, p.nbit);
+    p.acc_in = first ? 0 : 1;
+    p.g = g;
+    p.t = t;
+    LCH_TRY(cu(launch_gather<R>(p, ngroups, s)));
+    c->launches++;
+    first = false;
+  }
+  if (first)  // lgH_in == 0: the derivative of a constant is zero
+    return cu(cudaMemsetAsync(t, 0, bs_bytes(R, batch, lgH_out), s));
+  return LCH_OK;
+}
+
+template <class Fn>
+int dispatch(lch_ctx *c, Fn &&fn) {
+  if (c->t.r == 16 && c->t.poly == 0x1100Bu)
+    return fn(std::integral_constant<int, 16>{}, std::integral_constant<uint32_t, 0x1100Bu>{});
+  if (c->t.r == 8 && c->t.poly == 0x11Du)
+    return fn(std::integral_constant<int, 8>{}, std::integral_constant<uint32_t, 0x11Du>{});
+  return LCH_EUNSUPPORTED;
+}
+
+uint32_t hs_of(const lch_ctx *c, int level, uint32_t shift) {
+  return shift ? c->t.eval_w_hat(level, shift) : 0u;
+}
+
+int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out, uint16_t *log_out,
+                 cudaStream_t s) {
+  const int r = c->t.r;
+  const size_t n = size_t(1) << r;
+  Scratch sc(s);
+  uint32_t *buf = nullptr;
+  LCH_TRY(sc.alloc(buf, size_t(np) * n));
+  const int ngrp = (r + 7) / 8;
+  for (int rep = 0; rep < 2; ++rep) {
+    for (int gi = 0; gi < ngrp; ++gi) {
+      FwhtParams p;
+      std::memset(&p, 0, sizeof(p));
+      p.data = buf;
+      p.nvec = np;
+      p.lgn = r;
+      p.b0 = gi * 8;
+      p.tb = std::min(8, r - p.b0);
+      p.mod = c->t.m;
+      if (rep == 0 && gi == 0) p.bits = bits;
+      if (rep == 0 && gi == ngrp - 1) p.post_mul = c->d_fwht_log;
+      if (rep == 1 && gi == ngrp - 1) {
+        p.exp = c->d_exp;
+        p.loc_out = loc_out;
+        p.log_out = log_out;
+      }
+      LCH_TRY(cu(launch_fwht(p, s)));
+      c->launches++;
+    }
+  }
+  return LCH_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char *lch_version(void) { return "lch-b200 0.1 (sm_100a, bit-sliced)"; }
+
+const char *lch_strerror(int code) {
+  switch (code) {
+    case LCH_OK: return "ok";
+    case LCH_EINVAL: return "invalid argument";
+    case LCH_ETOOMANY: return "too many erasures";
+    case LCH_ENOTPRIM: return "reduction polynomial is not primitive";
+    case LCH_ECUDA: return "CUDA error or no CUDA device";
+    case LCH_ENOMEM: return "out of memory";
+    case LCH_EUNSUPPORTED: return "unsupported configuration";
+    case LCH_EZERODIV: return "division by zero";
+    default: return "unknown error";
+  }
+}
+
+int lch_init(int r, uint32_t poly, int max_lg_h, lch_ctx **out) {
+  if (!out) return LCH_EINVAL;
+  *out = nullptr;
+  if (max_lg_h < 0 || max_lg_h > 16) return LCH_EINVAL;
+  lch_ctx *c = new (std::nothrow) lch_ctx();
+  if (!c) return LCH_ENOMEM;
+  int rc = build_tables(r, poly, 1u << max_lg_h, c->t);
+  if (rc != LCH_OK) {
+    delete c;
+    return rc;
+  }
+  c->max_lg_h = max_lg_h;
+  *out = c;
+  return LCH_OK;
+}
+
+void lch_destroy(lch_ctx *c) {
+  if (!c) return;
+  if (c->dev_ready) {
+    cudaFree(c->d_w_hat);
+    cudaFree(c->d_b_prod);
+    cudaFree(c->d_b_prod_inv);
+    cudaFree(c->d_exp);
+    cudaFree(c->d_log);
+    cudaFree(c->d_fwht_log);
+  }
+  delete c;
+}
+
+int lch_get_tables(const lch_ctx *c, uint16_t *log, uint16_t *exp, uint16_t *w_hat,
+                   uint16_t *w_prime, uint16_t *b_prod, uint16_t *b_prod_inv, uint32_t *fwht_log,
+                   uint16_t *w_on_basis, uint16_t *w_norm) {
+  if (!c) return LCH_EINVAL;
+  const Tables &t = c->t;
+  if (log) std::memcpy(log, t.log.data(), t.order * 2);
+  if (exp) std::memcpy(exp, t.exp.data(), t.m * 2);
+  if (w_hat && !t.w_hat.empty()) std::memcpy(w_hat, t.w_hat.data(), t.w_hat.size() * 2);
+  if (w_prime) std::memcpy(w_prime, t.w_prime.data(), t.r * 2);
+  if (b_prod) std::memcpy(b_prod, t.b_prod.data(), t.max_h * 2);
+  if (b_prod_inv) std::memcpy(b_prod_inv, t.b_prod_inv.data(), t.max_h * 2);
+  if (fwht_log) std::memcpy(fwht_log, t.fwht_log.data(), t.order * 4);
+  if (w_on_basis) std::memcpy(w_on_basis, t.w_on_basis.data(), t.r * t.r * 2);
+  if (w_norm) std::memcpy(w_norm, t.w_norm.data(), t.r * 2);
+  return LCH_OK;
+}
+
+int64_t lch_launch_count(const lch_ctx *c) { return c ? c->launches : 0; }
+
+static int transform_impl(lch_ctx *c, uint16_t *data, int64_t batch, int64_t stride, int lg_h,
+                          uint32_t shift, int64_t packet_len, void *stream, bool inverse) {
+  if (!c || lg_h < 0 || lg_h > c->max_lg_h || batch < 0) return LCH_EINVAL;
+  if (shift >= c->t.order) return LCH_EINVAL;
+  if (packet_len != 0) return LCH_EUNSUPPORTED;
+  const int64_t h = int64_t(1) << lg_h;
+  if (stride < h) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || lg_h == 0) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<LOp> ops;
+  if (inverse)
+    for (int i = 0; i < lg_h; ++i) ops.push_back({OP_INV, i, hs_of(c, i, shift), nullptr});
+  else
+    for (int i = lg_h - 1; i >= 0; --i) ops.push_back({OP_FWD, i, hs_of(c, i, shift), nullptr});
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    auto plan = plan_passes(ops, lg_h, true, true);
+    RawIO io = make_raw(data, stride);
+    Scratch sc(s);
+    uint4 *work = nullptr;
+    if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, batch, lg_h) / 16));
+    return run_plan<R, P>(c, plan, lg_h, batch, &io, nullptr, &io, work, s);
+  });
+}
+
+int lch_forward(lch_ctx *c, uint16_t *data, int64_t batch, int64_t stride, int lg_h, uint32_t shift,
+                int64_t packet_len, void *stream) {
+  return transform_impl(c, data, batch, stride, lg_h, shift, packet_len, stream, false);
+}
+
+int lch_inverse(lch_ctx *c, uint16_t *data, int64_t batch, int64_t stride, int lg_h, uint32_t shift,
+                int64_t packet_len, void *stream) {
+  return transform_impl(c, data, batch, stride, lg_h, shift, packet_len, stream, true);
+}
+
+int lch_derivative(lch_ctx *c, const uint16_t *in, uint16_t *out, int64_t batch, int64_t stride,
+                   int lg_h, int64_t packet_len, void *stream) {
+  if (!c || lg_h < 0 || lg_h > c->max_lg_h || batch < 0) return LCH_EINVAL;
+  if (packet_len != 0) return LCH_EUNSUPPORTED;
+  const int64_t h = int64_t(1) << lg_h;
+  if (stride < h) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (lg_h == 0)
+    return cu(cudaMemset2DAsync(out, size_t(stride) * 2, 0, 2, size_t(batch), s));
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    Scratch sc(s);
+    uint4 *x = nullptr, *t = nullptr;
+    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, lg_h) / 16));
+    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, lg_h) / 16));
+    RawIO in_io = make_raw(const_cast<uint16_t *>(in), stride);
+    RawIO out_io = make_raw(out, stride);
+    // derivative.py:56 scale by B_i, :60-70 gather-XOR, :73-76 scale by B_j^-1
+    std::vector<LOp> pre = {{OP_SCALE, 0, 0, c->d_b_prod}};
+    LCH_TRY((run_plan<R, P>(c, plan_passes(pre, lg_h, true, false), lg_h, batch, &in_io, nullptr,
+                            nullptr, x, s)));
+    LCH_TRY(run_gather<R>(c, x, t, lg_h, lg_h, batch, s));
+    std::vector<LOp> post = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
+    return run_plan<R, P>(c, plan_passes(post, lg_h, false, true), lg_h, batch, nullptr, t, &out_io,
+                          t, s);
+  });
+}
+
+int lch_fwht(lch_ctx *c, uint32_t *data, int64_t batch, int lg_n, uint32_t modulus, void *stream) {
+  if (!c || lg_n < 0 || lg_n > 24 || batch < 0 || modulus == 0) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int b0 = 0;
+  do {
+    FwhtParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.data = data;
+    p.nvec = batch;
+    p.lgn = lg_n;
+    p.b0 = b0;
+    p.tb = std::min(8, lg_n - b0);
+    p.mod = modulus;
+    LCH_TRY(cu(launch_fwht(p, s)));
+    c->launches++;
+    b0 += 8;
+  } while (b0 < lg_n);
+  return LCH_OK;
+}
+
+int lch_locator(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out, uint16_t *log_out,
+                void *stream) {
+  if (!c || np < 0 || !bits) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (np == 0) return LCH_OK;
+  return locator_impl(c, bits, np, loc_out, log_out, static_cast<cudaStream_t>(stream));
+}
+
+int lch_encode(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
+               int64_t stride_out, int64_t batch, int lg_k, int64_t packet_len, void *stream) {
+  if (!c || batch < 0 || lg_k < 0 || lg_k > c->t.r) return LCH_EINVAL;
+  if (lg_k > c->max_lg_h) return LCH_EINVAL;  // rs.py:162-163
+  if (packet_len != 0) return LCH_EUNSUPPORTED;
+  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k, nb = n / k;
+  if (stride_in < k || (nb > 1 && stride_out < n - k)) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || nb == 1) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (lg_k == 0) {
+    // 1-point transforms are the identity: every parity symbol is the message
+    for (int64_t i = 1; i < nb; ++i)
+      LCH_TRY(cu(cudaMemcpy2DAsync(parity + (i - 1), size_t(stride_out) * 2, msg, size_t(stride_in) * 2,
+                                   2, size_t(batch), cudaMemcpyDeviceToDevice, s)));
+    return LCH_OK;
+  }
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    Scratch sc(s);
+    RawIO in_io = make_raw(const_cast<uint16_t *>(msg), stride_in);
+    // rs.py:91 coefficients by a k-point inverse at shift 0
+    std::vector<LOp> inv;
+    for (int i = 0; i < lg_k; ++i) inv.push_back({OP_INV, i, 0u, nullptr});
+    if (nb == 2) {
+      // rs.py:93-95 with one parity block: fuse inverse and forward(shift k)
+      std::vector<LOp> ops = inv;
+      for (int i = lg_k - 1; i >= 0; --i) ops.push_back({OP_FWD, i, hs_of(c, i, uint32_t(k)), nullptr});
+      auto plan = plan_passes(ops, lg_k, true, true);
+      uint4 *work = nullptr;
+      if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, batch, lg_k) / 16));
+      RawIO out_io = make_raw(parity, stride_out);
+      return run_plan<R, P>(c, plan, lg_k, batch, &in_io, nullptr, &out_io, work, s);
+    }
+    uint4 *coef = nullptr, *work = nullptr;
+    LCH_TRY(sc.alloc(coef, bs_bytes(R, batch, lg_k) / 16));
+    LCH_TRY(sc.alloc(work, bs_bytes(R, batch, lg_k) / 16));
+    LCH_TRY((run_plan<R, P>(c, plan_passes(inv, lg_k, true, false), lg_k, batch, &in_io, nullptr,
+                            nullptr, coef, s)));
+    for (int64_t blk = 1; blk < nb; ++blk) {
+      std::vector<LOp> fwd;
+      const uint32_t shift = uint32_t(blk * k);
+      for (int i = lg_k - 1; i >= 0; --i) fwd.push_back({OP_FWD, i, hs_of(c, i, shift), nullptr});
+      RawIO out_io = make_raw(parity + (blk - 1) * k, stride_out);
+      LCH_TRY((run_plan<R, P>(c, plan_passes(fwd, lg_k, false, true), lg_k, batch, nullptr, coef,
+                              &out_io, work, s)));
+    }
+    return LCH_OK;
+  });
+}
+
+int lch_decode(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t *bits, int shared,
+               uint16_t *out, int64_t stride_out, int64_t batch, int lg_k, int64_t packet_len,
+               const int64_t *host_counts, void *stream) {
+  if (!c || batch < 0 || lg_k < 0 || lg_k > c->t.r || !bits) return LCH_EINVAL;
+  if (lg_k > c->max_lg_h) return LCH_EINVAL;
+  if (packet_len != 0) return LCH_EUNSUPPORTED;
+  const int r = c->t.r;
+  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k;
+  if (stride_in < n || stride_out < k) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0) return LCH_OK;
+  if (!shared) return LCH_EUNSUPPORTED;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int64_t count = 0;
+  if (host_counts) {
+    count = host_counts[0];
+  } else {
+    Scratch sc(s);
+    int64_t *dcount = nullptr;
+    LCH_TRY(sc.alloc(dcount, 1));
+    LCH_TRY(cu(launch_count_bits(bits, 1, int(n / 32 > 0 ? n / 32 : 1), dcount, s)));
+    c->launches++;
+    LCH_TRY(cu(cudaMemcpyAsync(&count, dcount, sizeof(int64_t), cudaMemcpyDeviceToHost, s)));
+    LCH_TRY(cu(cudaStreamSynchronize(s)));
+  }
+  if (count == 0)  // rs.py:119-120
+    return cu(cudaMemcpy2DAsync(out, size_t(stride_out) * 2, rx, size_t(stride_in) * 2, size_t(k) * 2,
+                                size_t(batch), cudaMemcpyDeviceToDevice, s));
+  if (count > n - k) return LCH_ETOOMANY;  // rs.py:121-123
+  if (c->max_lg_h < r) return LCH_EINVAL;  // n-point transforms (transform.py:63-64)
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    Scratch sc(s);
+    uint16_t *logs = nullptr, *pi_row = nullptr, *pinv = nullptr;
+    LCH_TRY(sc.alloc(logs, size_t(n)));
+    LCH_TRY(sc.alloc(pi_row, size_t(n)));
+    LCH_TRY(sc.alloc(pinv, size_t(k)));
+    // rs.py:125 locator values for the shared pattern
+    LCH_TRY(locator_impl(c, bits, 1, nullptr, logs, s));
+    LCH_TRY(cu(launch_decode_rows(logs, bits, c->d_exp, c->t.m, uint32_t(n), uint32_t(k), pi_row,
+                                  pinv, s)));
+    c->launches++;
+    uint4 *x = nullptr, *t = nullptr;
+    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, r) / 16));
+    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, std::max(lg_k, 1)) / 16));
+    RawIO in_io = make_raw(const_cast<uint16_t *>(rx), stride_in);
+    // rs.py:130-136: phi = received * Pi_bar, n-point inverse; derivative.py:56 B scaling
+    std::vector<LOp> a = {{OP_SCALE, 0, 0, pi_row}};
+    for (int i = 0; i < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
+    a.push_back({OP_SCALE, 0, 0, c->d_b_prod});
+    LCH_TRY((run_plan<R, P>(c, plan_passes(a, r, true, false), r, batch, &in_io, nullptr, nullptr, x, s)));
+    // derivative.py:60-70 gather, only the first k coefficients are needed
+    const int lgk_out = std::max(lg_k, 1);
+    LCH_TRY(run_gather<R>(c, x, t, r, lgk_out, batch, s));
+    // rs.py:137-148: B^-1 scaling, k-point forward (the first k evaluations of
+    // the n-point forward), division by Pi' on erased positions, survivors copied
+    std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
+    for (int i = lg_k - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
+    if (lg_k == 0) {
+      // 1-point forward = identity; produce 2 columns into a temp, keep column 0
+      uint16_t *tmp = nullptr;
+      LCH_TRY(sc.alloc(tmp, size_t(batch) * 8));
+      uint16_t *pinv2 = nullptr;
+      LCH_TRY(sc.alloc(pinv2, 2));
+      LCH_TRY(cu(cudaMemsetAsync(pinv2, 0, 4, s)));
+      LCH_TRY(cu(cudaMemcpyAsync(pinv2, pinv, 2, cudaMemcpyDeviceToDevice, s)));
+      b.push_back({OP_SCALE, 0, 0, pinv2});
+      RawIO out_io = make_raw(tmp, 8);
+      out_io.merge_src = rx;
+      out_io.merge_stride = stride_in;
+      out_io.merge_bits = bits;
+      out_io.vec = 0;
+      LCH_TRY((run_plan<R, P>(c, plan_passes(b, 1, false, true), 1, batch, nullptr, t, &out_io, t, s)));
+      return cu(cudaMemcpy2DAsync(out, size_t(stride_out) * 2, tmp, 16, 2, size_t(batch),
+                                  cudaMemcpyDeviceToDevice, s));
+    }
+    b.push_back({OP_SCALE, 0, 0, pinv});
+    RawIO out_io = make_raw(out, stride_out);
+    out_io.merge_src = rx;
+    out_io.merge_stride = stride_in;
+    out_io.merge_bits = bits;
+    out_io.vec = out_io.vec && (reinterpret_cast<uintptr_t>(rx) % 16 == 0) && (stride_in % 8 == 0);
+    return run_plan<R, P>(c, plan_passes(b, lg_k, false, true), lg_k, batch, nullptr, t, &out_io, t, s);
+  });
+}
+
+int lch_gen_symbols(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len, uint16_t *out,
+                    int64_t stride, void *stream) {
+  if (!c || batch < 0 || len < 0 || stride < len) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || len == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_gen_symbols(seed, cw0, batch, len, c->t.m, out, stride,
+                               static_cast<cudaStream_t>(stream)));
+}
+
+int lch_gen_keys(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len, int64_t *keys,
+                 void *stream) {
+  if (!c || batch < 0 || len < 0) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || len == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_gen_keys(seed, cw0, batch, len, keys, static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// Kernel parameter blocks and launchers (device side in lch_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lch {
+
+constexpr int NT = 256;        // threads per CTA (8 warps)
+constexpr int NWARP = NT / 32;
+constexpr int TPB_MAX = 5;     // tile = 2^5 positions x 1024 batch lanes
+constexpr int GROUP = 1024;    // batch lanes per CTA: 32 threads x 32 bits
+constexpr int MAXOPS = 24;
+
+enum OpKind : int { OP_FWD = 0, OP_INV = 1, OP_SCALE = 2 };
+enum IoMode : int { IO_BS = 0, IO_RAW = 1 };
+
+struct PassOp {
+  int kind;
+  int m;                  // local tile bit (FWD/INV)
+  int level;              // global butterfly level i
+  uint32_t hs;            // W^_i(shift) (0 for shift 0)
+  const uint16_t *table;  // per-position factors (SCALE), indexed by position
+};
+
+// Raw uint16 batch: element (b, j) at ptr[b * row_stride + j].
+// Decode epilogue: if merge_src, out(b, j) = erased(j) ? computed : merge_src(b, j)
+// with erased(j) = bit j of merge_bits.
+struct RawIO {
+  uint16_t *ptr;
+  int64_t row_stride;
+  const uint16_t *merge_src;
+  int64_t merge_stride;
+  const uint32_t *merge_bits;
+  int vec;  // 16-byte vector accesses allowed
+};
+
+struct PassParams {
+  int nops;
+  PassOp ops[MAXOPS];
+  int tpb;               // tile bits
+  int gbit[TPB_MAX];     // tile bit m -> global position bit
+  int lgH;               // positions in the buffers = 2^lgH
+  int nnb;               // non-tile bits
+  int nbit[16];          // non-tile bit i -> global position bit
+  int64_t batch;
+  int in_mode, out_mode;
+  const uint4 *bs_in;    // BS buffers: block (g, pos) = 32*R words at ((g << lgH) + pos) * 8R uint4
+  uint4 *bs_out;
+  RawIO raw_in, raw_out;
+  const uint16_t *w_hat;
+  uint32_t w_hat_off[17];
+};
+
+struct GatherParams {
+  int tpb;
+  int gbit[TPB_MAX];
+  int lgH_in, lgH_out;   // g has 2^lgH_in positions, T has 2^lgH_out (prefix)
+  int nnb;
+  int nbit[16];
+  int acc_in;            // accumulate into existing T
+  const uint4 *g;
+  uint4 *t;
+};
+
+struct FwhtParams {
+  uint32_t *data;        // [nvec][2^lgn]
+  int64_t nvec;
+  int lgn, b0, tb;       // this pass covers bits [b0, b0 + tb)
+  uint32_t mod;
+  const uint32_t *bits;  // indicator input (bitmask) when non-null
+  const uint32_t *post_mul;  // multiply by post_mul[j] mod after the pass
+  // epilogue (locator): loc = exp[x], log = x
+  const uint16_t *exp;
+  uint16_t *loc_out, *log_out;
+};
+
+template <int R, uint32_t POLY>
+cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s);
+template <int R>
+cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s);
+cudaError_t launch_fwht(const FwhtParams &p, cudaStream_t s);
+cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const uint16_t *exp,
+                               uint32_t m, uint32_t n, uint32_t k, uint16_t *pi_row,
+                               uint16_t *pinv, cudaStream_t s);
+cudaError_t launch_gen_symbols(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
+                               uint32_t mask, uint16_t *out, int64_t row_stride,
+                               cudaStream_t s);
+cudaError_t launch_gen_keys(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
+                            int64_t *keys, cudaStream_t s);
+cudaError_t launch_count_bits(const uint32_t *bits, int64_t npatterns, int words,
+                              int64_t *counts, cudaStream_t s);
+
+size_t pass_smem_bytes(int R, int tpb, bool raw);
+
+}  // namespace lch

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -99,8 +100,9 @@ struct LOp {
 };
 
 struct Plan {
-  std::vector<LOp> ops;
-  std::vector<int> bits;  // sorted tile bits
+  std::vector<LOp> pre, bf, post;  // scalings before, butterflies, scalings after
+  std::vector<int> bits;           // sorted tile bits
+  bool empty() const { return pre.empty() && bf.empty() && post.empty(); }
 };
 
 bool low_bits_only(const std::vector<int> &bits, int tpb) {
@@ -109,26 +111,37 @@ bool low_bits_only(const std::vector<int> &bits, int tpb) {
   return true;
 }
 
+// Group ops into passes: each pass = [scalings] [butterflies on <= TPB_MAX
+// distinct bits] [scalings].  The first/last pass touching a raw uint16
+// buffer must tile the contiguous low bits; empty transpose passes are added
+// when the op sequence starts/ends on high bits.
 std::vector<Plan> plan_passes(const std::vector<LOp> &ops, int lgH, bool raw_in, bool raw_out) {
   const int tpb = std::min(TPB_MAX, lgH);
   std::vector<Plan> out;
   Plan cur;
   auto has = [](const std::vector<int> &v, int b) { return std::find(v.begin(), v.end(), b) != v.end(); };
+  auto flush = [&]() {
+    out.push_back(cur);
+    cur = Plan();
+  };
   for (const LOp &op : ops) {
-    if (op.kind != OP_SCALE && !has(cur.bits, op.level)) {
-      if (int(cur.bits.size()) == tpb) {
-        out.push_back(cur);
-        cur = Plan();
+    if (op.kind == OP_SCALE) {
+      if (cur.bf.empty()) {
+        if (int(cur.pre.size()) == MAXSCALE) flush();
+        cur.pre.push_back(op);
+      } else {
+        if (int(cur.post.size()) == MAXSCALE) flush();
+        (cur.bf.empty() ? cur.pre : cur.post).push_back(op);
       }
-      cur.bits.push_back(op.level);
+      continue;
     }
-    cur.ops.push_back(op);
-    if (int(cur.ops.size()) == MAXOPS) {
-      out.push_back(cur);
-      cur = Plan();
-    }
+    if (!cur.post.empty()) flush();
+    if (!has(cur.bits, op.level) && int(cur.bits.size()) == tpb) flush();
+    if (int(cur.bf.size()) == MAXOPS) flush();
+    if (!has(cur.bits, op.level)) cur.bits.push_back(op.level);
+    cur.bf.push_back(op);
   }
-  if (!cur.ops.empty() || out.empty()) out.push_back(cur);
+  if (!cur.empty() || out.empty()) out.push_back(cur);
   if (raw_in && !low_bits_only(out.front().bits, tpb)) out.insert(out.begin(), Plan());
   if (raw_out && !low_bits_only(out.back().bits, tpb)) out.push_back(Plan());
   for (size_t i = 0; i < out.size(); ++i) {
@@ -146,6 +159,68 @@ std::vector<Plan> plan_passes(const std::vector<LOp> &ops, int lgH, bool raw_in,
   return out;
 }
 
+// Butterflies of a pass -> radix-4 rounds over <= 2 local tile bits.
+int build_rounds(const Plan &pl, PassParams &p) {
+  const int tpb = int(pl.bits.size());
+  auto local = [&](int level) {
+    return int(std::find(pl.bits.begin(), pl.bits.end(), level) - pl.bits.begin());
+  };
+  p.nops = 0;
+  p.nrounds = 0;
+  PassRound cur{};
+  cur.m0 = cur.m1 = -1;
+  auto close = [&]() -> int {
+    if (cur.m0 < 0) return LCH_OK;
+    if (p.nrounds == MAXROUNDS) return LCH_EINVAL;
+    if (cur.m1 < 0 && tpb >= 2)
+      for (int b = 0; b < tpb; ++b)
+        if (b != cur.m0) { cur.m1 = b; break; }
+    cur.nw = 0;
+    for (int b = 0; b < tpb; ++b)
+      if (b != cur.m0 && b != cur.m1) cur.obit[cur.nw++] = b;
+    cur.op_end = p.nops;
+    p.rounds[p.nrounds++] = cur;
+    cur = PassRound{};
+    cur.m0 = cur.m1 = -1;
+    return LCH_OK;
+  };
+  // Count the distinct-bit runs; with an odd number of levels the FIRST round
+  // takes a single level so the last round (which overlaps the next tile's
+  // loads) keeps two.
+  int nlev = 0;
+  {
+    int prev = -1;
+    for (const LOp &op : pl.bf)
+      if (local(op.level) != prev) ++nlev, prev = local(op.level);
+  }
+  bool single_first = (nlev % 2) == 1 && nlev > 1;
+  for (const LOp &op : pl.bf) {
+    const int mb = local(op.level);
+    if (cur.m0 < 0) {
+      cur.m0 = mb;
+      cur.op_begin = p.nops;
+    } else if (mb != cur.m0 && cur.m1 < 0 && !single_first) {
+      cur.m1 = mb;
+    } else if ((mb != cur.m0 && mb != cur.m1) ||
+               (mb == cur.m0 && cur.m1 >= 0 && p.nops > cur.op_begin &&
+                p.ops[p.nops - 1].m == 1)) {
+      // new round: a third bit, or a return from m1 to m0 (rounds are m0* m1*)
+      LCH_TRY(close());
+      single_first = false;
+      cur.m0 = mb;
+      cur.op_begin = p.nops;
+    }
+    PassOp &o = p.ops[p.nops++];
+    o.kind = op.kind;
+    o.level = op.level;
+    o.hs = op.hs;
+    o.table = nullptr;
+    o.m = (mb == cur.m0) ? 0 : 1;
+    o.mloc = mb;
+  }
+  return close();
+}
+
 void fill_bits(const std::vector<int> &bits, int lgH, int *gbit, int &nnb, int *nbit) {
   for (size_t m = 0; m < bits.size(); ++m) gbit[m] = bits[m];
   nnb = 0;
@@ -158,6 +233,7 @@ RawIO make_raw(uint16_t *ptr, int64_t stride) {
   io.ptr = ptr;
   io.row_stride = stride;
   io.vec = (reinterpret_cast<uintptr_t>(ptr) % 16 == 0) && (stride % 8 == 0);
+  io.al4 = (reinterpret_cast<uintptr_t>(ptr) % 4 == 0) && (stride % 2 == 0);
   return io;
 }
 
@@ -169,21 +245,16 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     const Plan &pl = plan[i];
     PassParams p;
     std::memset(&p, 0, sizeof(p));
-    p.nops = int(pl.ops.size());
-    for (int o = 0; o < p.nops; ++o) {
-      const LOp &op = pl.ops[o];
-      p.ops[o].kind = op.kind;
-      p.ops[o].level = op.level;
-      p.ops[o].hs = op.hs;
-      p.ops[o].table = op.table;
-      p.ops[o].m = 0;
-      if (op.kind != OP_SCALE)
-        p.ops[o].m = int(std::find(pl.bits.begin(), pl.bits.end(), op.level) - pl.bits.begin());
-    }
+    LCH_TRY(build_rounds(pl, p));
+    p.npre = int(pl.pre.size());
+    p.npost = int(pl.post.size());
+    for (int o = 0; o < p.npre; ++o) p.pre[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.pre[o].table};
+    for (int o = 0; o < p.npost; ++o) p.post[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.post[o].table};
     p.tpb = int(pl.bits.size());
     p.lgH = lgH;
     fill_bits(pl.bits, lgH, p.gbit, p.nnb, p.nbit);
     p.batch = batch;
+    p.ngroups = ngroups;
     const bool first = i == 0, last = i + 1 == plan.size();
     p.in_mode = (first && raw_in) ? IO_RAW : IO_BS;
     p.out_mode = (last && raw_out) ? IO_RAW : IO_BS;
@@ -192,6 +263,10 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     p.bs_in = (first && bs_in) ? bs_in : work;
     p.bs_out = work;
     p.w_hat = c->d_w_hat;
+    {
+      static const int dbg = std::getenv("LCH_DBG_PASS") ? std::atoi(std::getenv("LCH_DBG_PASS")) : 0;
+      p.dbg = dbg;
+    }
     for (int l = 0; l <= c->t.levels && l < 17; ++l) p.w_hat_off[l] = c->t.w_hat_off[l];
     LCH_TRY(cu(launch_pass<R, POLY>(p, ngroups, s)));
     c->launches++;

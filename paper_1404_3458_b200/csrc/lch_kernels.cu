@@ -9,6 +9,8 @@
 // Input/output is either the raw uint16 batch (transposed to/from bit planes
 // in registers) or the bit-sliced intermediate buffer (straight 2 KB block
 // copies, laid out exactly like the shared-memory tile).
+#include <algorithm>
+
 #include "lch_device.cuh"
 #include "lch_kernels.h"
 
@@ -54,6 +56,63 @@ struct Blk {
   }
 };
 
+// --- TMA (bulk async copy) + mbarrier helpers -------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_add_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// generic-proxy smem accesses before -> async-proxy (TMA) writes after
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned bytes,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(void *smem_ptr, const void *gptr) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_ptr));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gptr));
@@ -62,31 +121,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;\n" ::);
 }
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-template <int R>
-__device__ __forceinline__ void load_tile_bs(const PassParams &p, uint4 *smem,
-                                             const uint32_t *tpos, int g, uint32_t base,
-                                             int TP) {
-  constexpr int U4 = Blk<R>::U4;
-  const uint4 *src = p.bs_in + ((size_t(g) << p.lgH) * U4);
-  for (int idx = threadIdx.x; idx < TP * U4; idx += NT) {
-    const int q = idx / U4, c = idx - q * U4;
-    cp_async16(smem + idx, src + size_t(base | tpos[q]) * U4 + c);
-  }
-  cp_async_wait_all();
-}
 
 template <int R>
 __device__ __forceinline__ void store_tile_bs(const PassParams &p, const uint4 *smem,
                                               const uint32_t *tpos, int g, uint32_t base,
                                               int TP) {
+  if (p.dbg & 5) return;
   constexpr int U4 = Blk<R>::U4;
   uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
   for (int idx = threadIdx.x; idx < TP * U4; idx += NT) {
@@ -95,110 +135,144 @@ __device__ __forceinline__ void store_tile_bs(const PassParams &p, const uint4 *
   }
 }
 
-// Raw (row-major uint16) -> bit-sliced tile.  Requires the tile to be the
-// contiguous run [base, base + TP).  Lane w, bit L of a plane word = codeword
-// g*1024 + 32L + w of the group.
+
+
+// Raw staging for row-major uint16 tiles (tile = contiguous run [base,
+// base + TP) of 1024 rows): 32-bit words w(row, cw) = positions (2cw, 2cw+1),
+// stored column-major, word column cw at [cw * 1024, cw * 1024 + 1024) with
+// the row index XOR-swizzled by 8 * ((cw >> 2) & 3) (conflict-free for both the
+// 4-column stores of a 16-byte row chunk and the transposing column reads).
+// A column is exactly the 4 KB the two BS blocks of positions 2cw, 2cw+1
+// occupy (R = 16), so one warp transposes a column in place; for R = 8 the
+// BS tile lives past the staging area.  Lane w, bit L of a plane word =
+// codeword g*1024 + 32L + w of the group.
+__device__ __forceinline__ int stage_idx(int r, int cw) {
+  return cw * GROUP + (r ^ (8 * ((cw >> 2) & 3)));
+}
+
 template <int R>
-__device__ __forceinline__ void load_tile_raw(const PassParams &p, uint4 *smem, int g,
-                                              uint32_t base, int TP) {
+__host__ __device__ constexpr int bs_offset_u4() {
+  return R == 16 ? 0 : GROUP * (1 << TPB_MAX) * 2 / 16;
+}
+// half-tile staging area for the bulk stores of the last round, after the tile
+template <int R>
+__host__ __device__ constexpr int stage_offset_u4() {
+  return bs_offset_u4<R>() + (1 << TPB_MAX) * 8 * R;
+}
+
+// Issue the loads of a tile: BS input asynchronously (cp.async, no wait),
+// raw input synchronously through registers into the staging layout.
+// BS input: thread 0 issues one 2 KB (R = 16) bulk copy per position block,
+// completing on `bar` (the caller waits on it).  The caller guarantees every
+// thread finished its shared-memory accesses to the tile (barrier) before.
+template <int R>
+__device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, const uint32_t *tpos,
+                                           int g, uint32_t base, int TP, uint64_t *bar) {
+  if (p.in_mode == IO_BS) {
+    // lane 0 of every warp issues the blocks q = warp, warp + 8, ...; thread 0
+    // supplies the barrier's single arrival
+    if ((threadIdx.x & 31) == 0) {
+      constexpr int U4 = Blk<R>::U4;
+      uint4 *bs = smem + bs_offset_u4<R>();
+      const uint4 *src = p.bs_in + ((size_t(g) << p.lgH) * U4);
+      const int w = threadIdx.x >> 5;
+      fence_proxy_async();
+      if (!(p.dbg & 9)) {
+        int nq = 0;
+        for (int q = w; q < TP; q += NWARP) ++nq;
+        if (nq) mbar_add_tx(bar, unsigned(nq * U4 * 16));
+        for (int q = w; q < TP; q += NWARP)
+          tma_load_1d(bs + q * U4, src + size_t(base | tpos[q]) * U4, U4 * 16, bar);
+      }
+      if (w == 0) mbar_arrive(bar);
+    }
+    return;
+  }
+  if (p.dbg & 9) return;
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int WPR = TP >> 1;  // 32-bit words (position pairs) per row
+  const int WPR = TP >> 1;
   const int64_t row0 = int64_t(g) * GROUP;
   const RawIO &io = p.raw_in;
   if (io.vec && TP >= 8) {
-    const int lcpr = p.tpb - 3;  // log2 of 16-byte chunks per row
-    for (int idx = tid; idx < (GROUP << lcpr); idx += NT) {
+    const int lcpr = p.tpb - 3;
+    for (int idx = threadIdx.x; idx < (GROUP << lcpr); idx += NT) {
       const int r = idx >> lcpr, c = idx & ((1 << lcpr) - 1);
       const int64_t b = row0 + r;
       uint4 val = make_uint4(0u, 0u, 0u, 0u);
       if (b < p.batch)
-        val = ldg_stream(reinterpret_cast<const uint4 *>(io.ptr + b * io.row_stride + base) + c);
-      const int sw = (r >> 1) & (WPR - 1);
-      uint32_t *row = rs + r * WPR;
-      row[(4 * c + 0) ^ sw] = val.x;
-      row[(4 * c + 1) ^ sw] = val.y;
-      row[(4 * c + 2) ^ sw] = val.z;
-      row[(4 * c + 3) ^ sw] = val.w;
+        val = __ldcs(reinterpret_cast<const uint4 *>(io.ptr + b * io.row_stride + base) + c);
+      rs[stage_idx(r, 4 * c + 0)] = val.x;
+      rs[stage_idx(r, 4 * c + 1)] = val.y;
+      rs[stage_idx(r, 4 * c + 2)] = val.z;
+      rs[stage_idx(r, 4 * c + 3)] = val.w;
     }
-  } else {
-    for (int idx = tid; idx < GROUP * WPR; idx += NT) {
+  } else {  // small tiles / unaligned rows: 2 x 16-bit loads per word
+    for (int idx = threadIdx.x; idx < GROUP * WPR; idx += NT) {
       const int r = idx / WPR, cw = idx - r * WPR;
       const int64_t b = row0 + r;
       uint32_t w = 0;
       if (b < p.batch) {
-        const uint16_t *s = io.ptr + b * io.row_stride + base + 2 * cw;
-        w = uint32_t(s[0]) | (uint32_t(s[1]) << 16);
+        const uint16_t *src = io.ptr + b * io.row_stride + base + 2 * cw;
+        w = uint32_t(src[0]) | (uint32_t(src[1]) << 16);
       }
-      rs[r * WPR + (cw ^ ((r >> 1) & (WPR - 1)))] = w;
+      rs[stage_idx(r, cw)] = w;
     }
   }
-  __syncthreads();
-  uint32_t keep[2][2][R];
+}
+
+// Raw staging -> bit-sliced tile, one word column per warp (in place).
+template <int R>
+__device__ __forceinline__ void finish_tile_raw(uint4 *smem, int TP) {
+  const uint32_t *rs = reinterpret_cast<const uint32_t *>(smem);
+  uint4 *bs = smem + bs_offset_u4<R>();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int WPR = TP >> 1;
+  for (int cw = warp; cw < WPR; cw += NWARP) {
+    uint32_t a[32];
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int cw = warp + s * NWARP;
-    if (cw < WPR) {
-      uint32_t a[32];
+    for (int L = 0; L < 32; ++L) a[L] = rs[stage_idx(32 * L + lane, cw)];
+    __syncwarp();
+    transpose32(a);
+    uint32_t lo[R], hi[R];
 #pragma unroll
-      for (int L = 0; L < 32; ++L) {
-        const int r = 32 * L + lane;
-        a[L] = rs[r * WPR + (cw ^ ((r >> 1) & (WPR - 1)))];
-      }
-      transpose32(a);
-#pragma unroll
-      for (int k = 0; k < R; ++k) {
-        keep[s][0][k] = a[k];
-        keep[s][1][k] = a[16 + k];
-      }
+    for (int k = 0; k < R; ++k) {
+      lo[k] = a[k];
+      hi[k] = a[16 + k];
     }
+    Blk<R>::store(bs + (2 * cw) * Blk<R>::U4, lane, lo);
+    Blk<R>::store(bs + (2 * cw + 1) * Blk<R>::U4, lane, hi);
   }
-  __syncthreads();
+}
+
+template <int R>
+__device__ __forceinline__ void column_to_words(const uint4 *bs, int cw, int lane, uint32_t (&a)[32]) {
+  uint32_t v0[R], v1[R];
+  Blk<R>::load(bs + (2 * cw) * Blk<R>::U4, lane, v0);
+  Blk<R>::load(bs + (2 * cw + 1) * Blk<R>::U4, lane, v1);
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int cw = warp + s * NWARP;
-    if (cw < WPR) {
-      Blk<R>::store(smem + (2 * cw) * Blk<R>::U4, lane, keep[s][0]);
-      Blk<R>::store(smem + (2 * cw + 1) * Blk<R>::U4, lane, keep[s][1]);
-    }
+  for (int k = 0; k < 16; ++k) {
+    a[k] = (k < R) ? v0[k < R ? k : 0] : 0u;
+    a[16 + k] = (k < R) ? v1[k < R ? k : 0] : 0u;
   }
+  transpose32(a);
 }
 
 template <int R>
 __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem, int g,
                                                uint32_t base, int TP) {
+  if (p.dbg & 5) return;
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
+  const uint4 *bs = smem + bs_offset_u4<R>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int WPR = TP >> 1;
   const int64_t row0 = int64_t(g) * GROUP;
   const RawIO &io = p.raw_out;
-  uint32_t keep[2][32];
+  for (int cw = warp; cw < WPR; cw += NWARP) {
+    uint32_t a[32];
+    column_to_words<R>(bs, cw, lane, a);
+    __syncwarp();
 #pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int cw = warp + s * NWARP;
-    if (cw < WPR) {
-      uint32_t v0[R], v1[R];
-      Blk<R>::load(smem + (2 * cw) * Blk<R>::U4, lane, v0);
-      Blk<R>::load(smem + (2 * cw + 1) * Blk<R>::U4, lane, v1);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        keep[s][k] = (k < R) ? v0[k < R ? k : 0] : 0u;
-        keep[s][16 + k] = (k < R) ? v1[k < R ? k : 0] : 0u;
-      }
-      transpose32(keep[s]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int cw = warp + s * NWARP;
-    if (cw < WPR) {
-#pragma unroll
-      for (int L = 0; L < 32; ++L) {
-        const int r = 32 * L + lane;
-        rs[r * WPR + (cw ^ ((r >> 1) & (WPR - 1)))] = keep[s][L];
-      }
-    }
+    for (int L = 0; L < 32; ++L) rs[stage_idx(32 * L + lane, cw)] = a[L];
   }
   __syncthreads();
   if (io.vec && TP >= 8) {
@@ -207,10 +281,8 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
       const int r = idx >> lcpr, c = idx & ((1 << lcpr) - 1);
       const int64_t b = row0 + r;
       if (b >= p.batch) continue;
-      const int sw = (r >> 1) & (WPR - 1);
-      const uint32_t *row = rs + r * WPR;
-      uint4 val = make_uint4(row[(4 * c + 0) ^ sw], row[(4 * c + 1) ^ sw],
-                             row[(4 * c + 2) ^ sw], row[(4 * c + 3) ^ sw]);
+      uint4 val = make_uint4(rs[stage_idx(r, 4 * c + 0)], rs[stage_idx(r, 4 * c + 1)],
+                             rs[stage_idx(r, 4 * c + 2)], rs[stage_idx(r, 4 * c + 3)]);
       const uint32_t pos0 = base + 8 * c;
       if (io.merge_src) {
         const uint32_t eb = (io.merge_bits[pos0 >> 5] >> (pos0 & 31)) & 0xFFu;
@@ -234,7 +306,7 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
       const int r = idx / WPR, cw = idx - r * WPR;
       const int64_t b = row0 + r;
       if (b >= p.batch) continue;
-      const uint32_t w = rs[r * WPR + (cw ^ ((r >> 1) & (WPR - 1)))];
+      const uint32_t w = rs[stage_idx(r, cw)];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t pos = base + 2 * cw + h;
@@ -250,87 +322,287 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
 }  // namespace
 
 template <int R, uint32_t POLY>
-__global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
+__device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *smem,
+                                            const uint32_t *tpos, uint32_t base, int TP) {
   using F = GF<R, POLY>;
   constexpr int U4 = Blk<R>::U4;
-  extern __shared__ uint4 smem[];
-  __shared__ uint32_t tpos[1 << TPB_MAX];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int TP = 1 << p.tpb;
-  const uint32_t t = blockIdx.x;
-  const int g = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
+  for (int q = warp; q < TP; q += NWARP) {
+    uint32_t v[R];
+    Blk<R>::load(smem + q * U4, lane, v);
+    for (int o = 0; o < nops; ++o) {
+      const uint32_t f = __shfl_sync(0xffffffffu, uint32_t(__ldg(ops[o].table + (base | tpos[q]))), 0);
+      uint32_t acc[R];
+      if (f) {
+        F::mul(acc, v, f);
+      } else {
+#pragma unroll
+        for (int b = 0; b < R; ++b) acc[b] = 0u;
+      }
+#pragma unroll
+      for (int b = 0; b < R; ++b) v[b] = acc[b];
+    }
+    Blk<R>::store(smem + q * U4, lane, v);
+  }
+}
 
-  uint32_t base = 0;
-  for (int i = 0; i < p.nnb; ++i) base |= ((t >> i) & 1u) << p.nbit[i];
+// One LCH butterfly on a pair of bit-sliced positions (u at the block's lower
+// half): forward transform.py:126-133 (u' = u + f v, v' = u' + v) or inverse
+// transform.py:165-169 (v' = u + v, u' = u + f v').  f is warp-uniform.
+template <int R, uint32_t POLY>
+__device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv) {
+  using F = GF<R, POLY>;
+  if (inv) F::xor_into(v, u);
+  if (f) {
+    uint32_t t[R];
+    F::mul(t, v, f);
+    F::xor_into(u, t);
+  }
+  if (!inv) F::xor_into(v, u);
+}
+
+// Butterfly factors of one tile (transform.py:112,123: w_hat[i][c >> (i+1)] ^
+// W^_i(shift), with c the u position): entry (op, q_u) of the tile's table.
+// Each thread owns <= 2 entries; fetch() issues the global loads, put()
+// writes them to shared memory later so their latency hides behind compute.
+struct FactorLoader {
+  static constexpr int PER = (MAXOPS * (1 << (TPB_MAX - 1)) + NT - 1) / NT;
+  uint32_t v[PER];
+  int slot[PER];
+  __device__ __forceinline__ void fetch(const PassParams &p, const uint32_t *tpos, uint32_t base) {
+    const int half = 1 << (p.tpb - 1 < 0 ? 0 : p.tpb - 1);
+    const int n = p.nops * half;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int e = threadIdx.x + k * NT;
+      slot[k] = -1;
+      if (p.tpb > 0 && e < n) {
+        const int o = e / half, pp = e - o * half;
+        const PassOp &op = p.ops[o];
+        const int m = op.mloc;
+        const int qu = ((pp >> m) << (m + 1)) | (pp & ((1 << m) - 1));
+        const int lvl = op.level;
+        v[k] = uint32_t(__ldg(p.w_hat + p.w_hat_off[lvl] + ((base | tpos[qu]) >> (lvl + 1)))) ^ op.hs;
+        slot[k] = o * (1 << TPB_MAX) + qu;
+      }
+    }
+  }
+  __device__ __forceinline__ void put(uint32_t *fac) const {
+#pragma unroll
+    for (int k = 0; k < PER; ++k)
+      if (slot[k] >= 0) fac[slot[k]] = v[k];
+  }
+};
+
+template <int R, uint32_t POLY>
+__global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
+  constexpr int U4 = Blk<R>::U4;
+  extern __shared__ uint4 smem[];
+  uint4 *const bsm = smem + bs_offset_u4<R>();
+  __shared__ uint32_t tpos[1 << TPB_MAX];
+  __shared__ uint32_t fac[2][MAXOPS * (1 << TPB_MAX)];
+  __shared__ __align__(8) uint64_t bar;
+  unsigned phase = 0;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp index through a shuffle: provably warp-uniform for the compiler, so
+  // the butterfly factors and their digit tests live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int TP = 1 << p.tpb;
+  const int ntile = 1 << (p.lgH - p.tpb);
+  const int total = ntile * p.ngroups;
+  int tl = blockIdx.x;
+  if (tl >= total) return;
   if (tid < TP) {
     uint32_t o = 0;
     for (int m = 0; m < p.tpb; ++m) o |= ((uint32_t(tid) >> m) & 1u) << p.gbit[m];
     tpos[tid] = o;
   }
+  auto base_of = [&](int lin) {
+    const uint32_t t = uint32_t(lin % ntile);
+    uint32_t b = 0;
+    for (int i = 0; i < p.nnb; ++i) b |= ((t >> i) & 1u) << p.nbit[i];
+    return b;
+  };
+  int g = tl / ntile;
+  uint32_t base = base_of(tl);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  issue_tile<R>(p, smem, tpos, g, base, TP, &bar);
+  int fb = 0;  // factor-table buffer of the current tile
+  {
+    FactorLoader fl;
+    fl.fetch(p, tpos, base);
+    fl.put(fac[0]);
+  }
+  if (p.in_mode == IO_BS) {
+    mbar_wait(&bar, phase);
+    phase ^= 1u;
+  }
   __syncthreads();
 
-  if (p.in_mode == IO_BS)
-    load_tile_bs<R>(p, smem, tpos, g, base, TP);
-  else
-    load_tile_raw<R>(p, smem, g, base, TP);
-  __syncthreads();
+  // The last round keeps its data in registers and stores it straight to the
+  // BS output, so the next tile's loads can stream into shared memory while
+  // it computes.
+  const bool reg_path = p.nrounds > 0 && p.npost == 0 && p.out_mode == IO_BS;
 
-  for (int o = 0; o < p.nops; ++o) {
-    const int kind = p.ops[o].kind;
-    if (kind == OP_SCALE) {
-      const uint16_t *tab = p.ops[o].table;
-      for (int q = warp; q < TP; q += NWARP) {
-        const uint32_t f = __ldg(tab + (base | tpos[q]));
-        uint32_t v[R], acc[R];
-        Blk<R>::load(smem + q * U4, lane, v);
-        if (f) {
-          F::mul(acc, v, f);
-        } else {
-#pragma unroll
-          for (int b = 0; b < R; ++b) acc[b] = 0u;
+  for (;;) {
+    const int next = tl + int(gridDim.x);
+    const bool has_next = next < total;
+    if (p.in_mode == IO_RAW) {
+      finish_tile_raw<R>(smem, TP);
+      __syncthreads();
+    }
+    if (p.npre) {
+      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP);
+      __syncthreads();
+    }
+    for (int rd = 0; rd < p.nrounds; ++rd) {
+      const PassRound &rr = p.rounds[rd];
+      const bool last_reg = reg_path && rd == p.nrounds - 1;
+      const int M0 = 1 << rr.m0;
+      const bool has1 = rr.m1 >= 0;
+      const int M1 = has1 ? (1 << rr.m1) : 0;
+      const bool active = warp < (1 << rr.nw);
+      int q0 = 0;
+      for (int j = 0; j < rr.nw; ++j) q0 |= ((warp >> j) & 1) << rr.obit[j];
+      uint32_t a0[R], a1[R], a2[R], a3[R];
+      if (active) {
+        Blk<R>::load(bsm + q0 * U4, lane, a0);
+        Blk<R>::load(bsm + (q0 | M0) * U4, lane, a1);
+        if (has1) {
+          Blk<R>::load(bsm + (q0 | M1) * U4, lane, a2);
+          Blk<R>::load(bsm + (q0 | M0 | M1) * U4, lane, a3);
         }
-        Blk<R>::store(smem + q * U4, lane, acc);
       }
-    } else {
-      const int m = p.ops[o].m, lvl = p.ops[o].level;
-      const uint32_t hs = p.ops[o].hs;
-      const uint16_t *hat = p.w_hat + p.w_hat_off[lvl];
-      for (int pp = warp; pp < (TP >> 1); pp += NWARP) {
-        const int qu = ((pp >> m) << (m + 1)) | (pp & ((1 << m) - 1));
-        const int qv = qu | (1 << m);
-        const uint32_t pos_u = base | tpos[qu];
-        const uint32_t f = __ldg(hat + (pos_u >> (lvl + 1))) ^ hs;
-        uint32_t u[R], v[R];
-        Blk<R>::load(smem + qu * U4, lane, u);
-        Blk<R>::load(smem + qv * U4, lane, v);
-        if (kind == OP_FWD) {
-          // transform.py:126-133: u' = u + f v, v' = u' + v
-          if (f) {
-            uint32_t fv[R];
-            F::mul(fv, v, f);
-            F::xor_into(u, fv);
+      FactorLoader nfl;
+      if (last_reg) {
+        __syncthreads();
+        if (has_next) {
+          const uint32_t nb = base_of(next);
+          issue_tile<R>(p, smem, tpos, next / ntile, nb, TP, &bar);
+          nfl.fetch(p, tpos, nb);
+        }
+      }
+      if (active) {
+        // A round's ops are [along m0]* [along m1]*.  Along m0 the pairs are
+        // (a0,a1), (a2,a3); at the first m1 op a1 and a2 swap once, so the same
+        // two inlined butterflies (one multiply body each) serve both bits.
+        bool sw = false;
+        for (int o = rr.op_begin; o < ((p.dbg & 2) ? rr.op_begin : rr.op_end); ++o) {
+          const PassOp &op = p.ops[o];
+          const bool inv = op.kind == OP_INV;
+          if (op.m == 1 && !sw) {
+#pragma unroll
+            for (int b = 0; b < R; ++b) {
+              const uint32_t x = a1[b];
+              a1[b] = a2[b];
+              a2[b] = x;
+            }
+            sw = true;
           }
-          F::xor_into(v, u);
-        } else {
-          // transform.py:165-169: v' = u + v, u' = u + f v'
-          F::xor_into(v, u);
-          if (f) {
-            uint32_t fv[R];
-            F::mul(fv, v, f);
-            F::xor_into(u, fv);
+          const uint32_t *ft = fac[fb] + o * (1 << TPB_MAX);
+          const uint32_t f1 = __shfl_sync(0xffffffffu, ft[q0], 0);
+          butterfly<R, POLY>(a0, a1, f1, inv);
+          if (has1) {
+            const uint32_t f2 = __shfl_sync(0xffffffffu, ft[sw ? (q0 | M0) : (q0 | M1)], 0);
+            butterfly<R, POLY>(a2, a3, f2, inv);
           }
         }
-        Blk<R>::store(smem + qu * U4, lane, u);
-        Blk<R>::store(smem + qv * U4, lane, v);
+        if (sw) {
+#pragma unroll
+          for (int b = 0; b < R; ++b) {
+            const uint32_t x = a1[b];
+            a1[b] = a2[b];
+            a2[b] = x;
+          }
+        }
+        if (!last_reg) {
+          Blk<R>::store(bsm + q0 * U4, lane, a0);
+          Blk<R>::store(bsm + (q0 | M0) * U4, lane, a1);
+          if (has1) {
+            Blk<R>::store(bsm + (q0 | M1) * U4, lane, a2);
+            Blk<R>::store(bsm + (q0 | M0 | M1) * U4, lane, a3);
+          }
+        }
+      }
+      if (last_reg && (p.dbg & 16)) {
+        // experiment: direct register -> global stores
+        if (active && !(p.dbg & 5)) {
+          uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
+          Blk<R>::store(dst + size_t(base | tpos[q0]) * U4, lane, a0);
+          Blk<R>::store(dst + size_t(base | tpos[q0 | M0]) * U4, lane, a1);
+          if (has1) {
+            Blk<R>::store(dst + size_t(base | tpos[q0 | M1]) * U4, lane, a2);
+            Blk<R>::store(dst + size_t(base | tpos[q0 | M0 | M1]) * U4, lane, a3);
+          }
+        }
+        if (has_next) nfl.put(fac[fb ^ 1]);
+      } else if (last_reg) {
+        // Drain the tile through the staging half-buffer with bulk stores
+        // (asynchronous: they overlap the next tile's rounds).
+        uint4 *stg = smem + stage_offset_u4<R>();
+        uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
+        const int HALF = TP >> 1;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (lane == 0) tma_store_wait_read();
+          __syncthreads();
+          if (active) {
+            const int qs[4] = {q0, q0 | M0, q0 | M1, q0 | M0 | M1};
+            if ((qs[0] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[0] & (HALF - 1)) * U4, lane, a0);
+            if ((qs[1] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[1] & (HALF - 1)) * U4, lane, a1);
+            if (has1) {
+              if ((qs[2] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[2] & (HALF - 1)) * U4, lane, a2);
+              if ((qs[3] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[3] & (HALF - 1)) * U4, lane, a3);
+            }
+          }
+          fence_proxy_async();
+          __syncthreads();
+          if (lane == 0 && !(p.dbg & 5)) {
+            for (int q = warp; q < HALF; q += NWARP)
+              tma_store_1d(dst + size_t(base | tpos[h * HALF + q]) * U4, stg + q * U4, U4 * 16);
+            tma_store_commit();
+          }
+        }
+        if (has_next) nfl.put(fac[fb ^ 1]);
+      }
+      if (!last_reg) __syncthreads();
+    }
+    if (!reg_path) {
+      if (p.npost) {
+        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP);
+        __syncthreads();
+      }
+      if (p.out_mode == IO_BS)
+        store_tile_bs<R>(p, bsm, tpos, g, base, TP);
+      else
+        store_tile_raw<R>(p, smem, g, base, TP);
+      __syncthreads();
+      if (has_next) {
+        const uint32_t nb = base_of(next);
+        issue_tile<R>(p, smem, tpos, next / ntile, nb, TP, &bar);
+        FactorLoader fl;
+        fl.fetch(p, tpos, nb);
+        fl.put(fac[fb ^ 1]);
       }
     }
+    if (!has_next) {
+      if (lane == 0) tma_store_wait_all();
+      break;
+    }
+    if (p.in_mode == IO_BS) {
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+    }
     __syncthreads();
+    fb ^= 1;
+    tl = next;
+    g = tl / ntile;
+    base = base_of(tl);
   }
-
-  if (p.out_mode == IO_BS)
-    store_tile_bs<R>(p, smem, tpos, g, base, TP);
-  else
-    store_tile_raw<R>(p, smem, g, base, TP);
 }
 
 // T[pos] (+)= XOR over tile bits m with bit m of q clear of g[pos | 2^gbit[m]],
@@ -494,10 +766,12 @@ __global__ void count_bits_kernel(const uint32_t *bits, int64_t npatterns, int w
 // ---------------------------------------------------------------------------
 
 size_t pass_smem_bytes(int R, int tpb, bool raw) {
-  const size_t tp = size_t(1) << tpb;
-  size_t bs = tp * 8 * R * 16;
-  size_t rw = raw ? size_t(GROUP) * tp * 2 : 0;
-  return bs > rw ? bs : rw;
+  // [raw staging (R = 8 only)] [BS tile] [half-tile bulk-store staging]
+  (void)tpb;
+  (void)raw;
+  const size_t tile = (size_t(1) << TPB_MAX) * 8 * R * 16;
+  const size_t pre = R == 16 ? 0 : size_t(GROUP) * (size_t(1) << TPB_MAX) * 2;
+  return pre + tile + tile / 2;
 }
 
 template <int R, uint32_t POLY>
@@ -512,8 +786,16 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(1u << (p.lgH - p.tpb), ngroups);
-  pass_kernel<R, POLY><<<grid, NT, smem, s>>>(p);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
+  const int64_t ctas = std::min<int64_t>(total, int64_t(2) * nsm);
+  pass_kernel<R, POLY><<<unsigned(ctas), NT, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -12,16 +12,29 @@ constexpr int NWARP = NT / 32;
 constexpr int TPB_MAX = 5;     // tile = 2^5 positions x 1024 batch lanes
 constexpr int GROUP = 1024;    // batch lanes per CTA: 32 threads x 32 bits
 constexpr int MAXOPS = 24;
+constexpr int MAXROUNDS = 12;
+constexpr int MAXSCALE = 4;
 
 enum OpKind : int { OP_FWD = 0, OP_INV = 1, OP_SCALE = 2 };
 enum IoMode : int { IO_BS = 0, IO_RAW = 1 };
 
 struct PassOp {
   int kind;
-  int m;                  // local tile bit (FWD/INV)
+  int m;                  // FWD/INV: which bit of the round (0 -> m0, 1 -> m1)
+  int mloc;               // FWD/INV: the op's local tile bit
   int level;              // global butterfly level i
   uint32_t hs;            // W^_i(shift) (0 for shift 0)
   const uint16_t *table;  // per-position factors (SCALE), indexed by position
+};
+
+// A round: every thread holds the 4 positions spanned by tile bits m0, m1
+// (radix-4, two levels per shared-memory round trip); the warp index
+// enumerates the remaining nw tile bits obit[].
+struct PassRound {
+  int m0, m1;             // local tile bits (m1 = -1: only m0 exists, tpb == 1)
+  int nw;
+  int obit[TPB_MAX];
+  int op_begin, op_end;   // butterfly ops of the round in ops[]
 };
 
 // Raw uint16 batch: element (b, j) at ptr[b * row_stride + j].
@@ -34,23 +47,30 @@ struct RawIO {
   int64_t merge_stride;
   const uint32_t *merge_bits;
   int vec;  // 16-byte vector accesses allowed
+  int al4;  // 4-byte aligned rows (asynchronous 32-bit staging copies)
 };
 
 struct PassParams {
   int nops;
   PassOp ops[MAXOPS];
+  int nrounds;
+  PassRound rounds[MAXROUNDS];
+  int npre, npost;        // per-position scalings before / after the rounds
+  PassOp pre[MAXSCALE], post[MAXSCALE];
   int tpb;               // tile bits
   int gbit[TPB_MAX];     // tile bit m -> global position bit
   int lgH;               // positions in the buffers = 2^lgH
   int nnb;               // non-tile bits
   int nbit[16];          // non-tile bit i -> global position bit
   int64_t batch;
+  int ngroups;           // 1024-lane batch groups
   int in_mode, out_mode;
   const uint4 *bs_in;    // BS buffers: block (g, pos) = 32*R words at ((g << lgH) + pos) * 8R uint4
   uint4 *bs_out;
   RawIO raw_in, raw_out;
   const uint16_t *w_hat;
   uint32_t w_hat_off[17];
+  int dbg;  // experiments only: 1 = skip global I/O, 2 = skip butterflies
 };
 
 struct GatherParams {

@@ -21,6 +21,7 @@ struct lch_ctx {
   int device = -1;
   uint16_t *d_w_hat = nullptr, *d_b_prod = nullptr, *d_b_prod_inv = nullptr;
   uint16_t *d_exp = nullptr, *d_log = nullptr;
+  uint16_t *d_b_lo = nullptr;  // b_prod[j mod 2^(r-1)] for j < 2^r (decode derivative)
   uint32_t *d_fwht_log = nullptr;
   int64_t launches = 0;
   std::mutex mu;
@@ -58,6 +59,11 @@ int ensure_device(lch_ctx *c) {
   LCH_TRY(upload(c->d_exp, c->t.exp));
   LCH_TRY(upload(c->d_log, c->t.log));
   LCH_TRY(upload(c->d_fwht_log, c->t.fwht_log));
+  if (c->t.max_h == c->t.order) {
+    std::vector<uint16_t> blo(c->t.order);
+    for (uint32_t j = 0; j < c->t.order; ++j) blo[j] = c->t.b_prod[j & (c->t.order / 2 - 1)];
+    LCH_TRY(upload(c->d_b_lo, blo));
+  }
   // keep freed scratch in the stream-ordered pool (no re-mapping per call)
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
@@ -239,7 +245,8 @@ RawIO make_raw(uint16_t *ptr, int64_t stride) {
 
 template <int R, uint32_t POLY>
 int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, const RawIO *raw_in,
-             const uint4 *bs_in, const RawIO *raw_out, uint4 *work, cudaStream_t s) {
+             const uint4 *bs_in, const RawIO *raw_out, uint4 *work, cudaStream_t s,
+             uint4 *gt_out = nullptr, int gt_lgH = 0) {
   const int ngroups = int((batch + GROUP - 1) / GROUP);
   for (size_t i = 0; i < plan.size(); ++i) {
     const Plan &pl = plan[i];
@@ -263,6 +270,10 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     p.bs_in = (first && bs_in) ? bs_in : work;
     p.bs_out = work;
     p.w_hat = c->d_w_hat;
+    if (last && gt_out) {
+      p.gt_out = gt_out;
+      p.gt_lgH = gt_lgH;
+    }
     {
       static const int dbg = std::getenv("LCH_DBG_PASS") ? std::atoi(std::getenv("LCH_DBG_PASS")) : 0;
       p.dbg = dbg;
@@ -279,31 +290,48 @@ size_t bs_bytes(int R, int64_t batch, int lgH) {
   return size_t(ngroups) * (size_t(1) << lgH) * 32 * R * 4;
 }
 
-template <int R>
-int run_gather(lch_ctx *c, const uint4 *g, uint4 *t, int lgH_in, int lgH_out, int64_t batch,
+// Derivative gather over the position bits `bits` (all except those already
+// summed), in passes of <= GMAXB bits; `special` (or -1) is the top bit
+// handled as c * (y[j] + y[j | 2^special]) (decode: folded top inverse level).
+template <int R, uint32_t POLY>
+int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, int64_t batch,
+               std::vector<int> bits, int special, uint32_t cconst, const uint4 *t_in,
                cudaStream_t s) {
-  // The kernel sums over every tile bit, so each pass's tile is exactly one
-  // group of <= TPB_MAX consecutive bits; the groups partition [0, lgH_in).
   const int ngroups = int((batch + GROUP - 1) / GROUP);
+  std::sort(bits.begin(), bits.end());
+  if (special >= 0) bits.erase(std::remove(bits.begin(), bits.end(), special), bits.end());
   bool first = true;
-  for (int b0 = 0; b0 < lgH_in; b0 += TPB_MAX) {
+  size_t i = 0;
+  do {
     GatherParams p;
     std::memset(&p, 0, sizeof(p));
-    std::vector<int> bits;
-    for (int b = b0; b < std::min(b0 + TPB_MAX, lgH_in); ++b) bits.push_back(b);
-    p.tpb = int(bits.size());
+    std::vector<int> grp;
+    const int room = GMAXB - (first && special >= 0 ? 1 : 0);
+    while (i < bits.size() && int(grp.size()) < room) grp.push_back(bits[i++]);
+    p.sb = -1;
+    if (first && special >= 0) {
+      grp.push_back(special);
+      std::sort(grp.begin(), grp.end());
+      p.sb = int(std::find(grp.begin(), grp.end(), special) - grp.begin());
+      p.c = cconst;
+    }
+    if (grp.empty()) break;
+    p.nbits = int(grp.size());
+    for (size_t m = 0; m < grp.size(); ++m) p.bits[m] = grp[m];
     p.lgH_in = lgH_in;
     p.lgH_out = lgH_out;
-    fill_bits(bits, lgH_in, p.gbit, p.nnb, p.nbit);
-    p.acc_in = first ? 0 : 1;
-    p.g = g;
-    p.t = t;
-    LCH_TRY(cu(launch_gather<R>(p, ngroups, s)));
+    fill_bits(grp, lgH_in, p.bits, p.nnb, p.nbit);
+    p.y = y;
+    p.t_in = first ? t_in : t;
+    p.t_out = t;
+    LCH_TRY(cu(launch_gather<R, POLY>(p, ngroups, s)));
     c->launches++;
     first = false;
-  }
-  if (first)  // lgH_in == 0: the derivative of a constant is zero
+  } while (i < bits.size());
+  if (first) {  // nothing to sum: T = T_in or 0
+    if (t_in) return cu(cudaMemcpyAsync(t, t_in, bs_bytes(R, batch, lgH_out), cudaMemcpyDeviceToDevice, s));
     return cu(cudaMemsetAsync(t, 0, bs_bytes(R, batch, lgH_out), s));
+  }
   return LCH_OK;
 }
 
@@ -399,6 +427,7 @@ void lch_destroy(lch_ctx *c) {
     cudaFree(c->d_exp);
     cudaFree(c->d_log);
     cudaFree(c->d_fwht_log);
+    cudaFree(c->d_b_lo);
   }
   delete c;
 }
@@ -483,7 +512,9 @@ int lch_derivative(lch_ctx *c, const uint16_t *in, uint16_t *out, int64_t batch,
     std::vector<LOp> pre = {{OP_SCALE, 0, 0, c->d_b_prod}};
     LCH_TRY((run_plan<R, P>(c, plan_passes(pre, lg_h, true, false), lg_h, batch, &in_io, nullptr,
                             nullptr, x, s)));
-    LCH_TRY(run_gather<R>(c, x, t, lg_h, lg_h, batch, s));
+    std::vector<int> all;
+    for (int b = 0; b < lg_h; ++b) all.push_back(b);
+    LCH_TRY((run_gather<R, P>(c, x, t, lg_h, lg_h, batch, all, -1, 0u, nullptr, s)));
     std::vector<LOp> post = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
     return run_plan<R, P>(c, plan_passes(post, lg_h, false, true), lg_h, batch, nullptr, t, &out_io,
                           t, s);
@@ -615,18 +646,30 @@ int lch_decode(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t
     LCH_TRY(cu(launch_decode_rows(logs, bits, c->d_exp, c->t.m, uint32_t(n), uint32_t(k), pi_row,
                                   pinv, s)));
     c->launches++;
-    uint4 *x = nullptr, *t = nullptr;
-    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, r) / 16));
-    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, std::max(lg_k, 1)) / 16));
-    RawIO in_io = make_raw(const_cast<uint16_t *>(rx), stride_in);
-    // rs.py:130-136: phi = received * Pi_bar, n-point inverse; derivative.py:56 B scaling
-    std::vector<LOp> a = {{OP_SCALE, 0, 0, pi_row}};
-    for (int i = 0; i < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
-    a.push_back({OP_SCALE, 0, 0, c->d_b_prod});
-    LCH_TRY((run_plan<R, P>(c, plan_passes(a, r, true, false), r, batch, &in_io, nullptr, nullptr, x, s)));
-    // derivative.py:60-70 gather, only the first k coefficients are needed
     const int lgk_out = std::max(lg_k, 1);
-    LCH_TRY(run_gather<R>(c, x, t, r, lgk_out, batch, s));
+    uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
+    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, r) / 16));
+    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, lgk_out) / 16));
+    LCH_TRY(sc.alloc(t1, bs_bytes(R, batch, lgk_out) / 16));
+    RawIO in_io = make_raw(const_cast<uint16_t *>(rx), stride_in);
+    // rs.py:130-136: phi = received * Pi_bar and the n-point inverse.  The top
+    // level r-1 is a pure XOR at shift 0 (its only block has factor 0) and is
+    // folded into the derivative below: with x the state after levels
+    // 0..r-2 and y_j = B_(j mod n/2) x_j, the derivative gather of
+    // derivative.py:56-70 for j < k is
+    //   T_j = W'_(r-1) (y_j + y_(j+n/2)) + sum_(l < r-1, bit l of j clear) y_(j | 2^l).
+    std::vector<LOp> a = {{OP_SCALE, 0, 0, pi_row}};
+    for (int i = 0; i + 1 < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
+    a.push_back({OP_SCALE, 0, 0, c->d_b_lo});
+    auto plan_a = plan_passes(a, r, true, false);
+    // the last inverse pass also sums the gather over its own tile bits
+    LCH_TRY((run_plan<R, P>(c, plan_a, r, batch, &in_io, nullptr, nullptr, x, s, t1, lgk_out)));
+    std::vector<int> rest;
+    for (int b = 0; b + 1 < r; ++b)
+      if (std::find(plan_a.back().bits.begin(), plan_a.back().bits.end(), b) == plan_a.back().bits.end())
+        rest.push_back(b);
+    rest.push_back(r - 1);
+    LCH_TRY((run_gather<R, P>(c, x, t, r, lgk_out, batch, rest, r - 1, c->t.w_prime[r - 1], t1, s)));
     // rs.py:137-148: B^-1 scaling, k-point forward (the first k evaluations of
     // the n-point forward), division by Pi' on erased positions, survivors copied
     std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};

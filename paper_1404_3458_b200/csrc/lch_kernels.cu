@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // The last round keeps its data in registers and stores it straight to the
   // BS output, so the next tile's loads can stream into shared memory while
   // it computes.
-  const bool reg_path = p.nrounds > 0 && p.npost == 0 && p.out_mode == IO_BS;
+  const bool reg_path = p.nrounds > 0 && p.npost == 0 && p.out_mode == IO_BS && !p.gt_out;
 
   for (;;) {
     const int next = tl + int(gridDim.x);
@@ -576,6 +576,26 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP);
         __syncthreads();
       }
+      if (p.gt_out) {
+        // derivative gather over the tile bits (derivative.py:60-70), for the
+        // output positions below 2^gt_lgH
+        uint4 *gdst = p.gt_out + ((size_t(g) << p.gt_lgH) * U4);
+        for (int q = warp; q < TP; q += NWARP) {
+          const uint32_t pos = base | tpos[q];
+          if (pos >= (1u << p.gt_lgH)) continue;
+          uint32_t acc[R];
+#pragma unroll
+          for (int b = 0; b < R; ++b) acc[b] = 0u;
+          for (int m = 0; m < p.tpb; ++m) {
+            if ((q >> m) & 1) continue;
+            uint32_t x[R];
+            Blk<R>::load(bsm + (q | (1 << m)) * U4, lane, x);
+#pragma unroll
+            for (int b = 0; b < R; ++b) acc[b] ^= x[b];
+          }
+          Blk<R>::store(gdst + size_t(pos) * U4, lane, acc);
+        }
+      }
       if (p.out_mode == IO_BS)
         store_tile_bs<R>(p, bsm, tpos, g, base, TP);
       else
@@ -605,58 +625,83 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   }
 }
 
-// T[pos] (+)= XOR over tile bits m with bit m of q clear of g[pos | 2^gbit[m]],
-// for pos < 2^lgH_out: the gather step of derivative.py:60-70, split by bit
-// groups so the full sum over all lg h bits takes ceil(lg h / tpb) passes.
-template <int R>
-__global__ void __launch_bounds__(NT, 2) gather_kernel(const __grid_constant__ GatherParams p) {
+template <int R, uint32_t POLY>
+__global__ void __launch_bounds__(NT) gather_kernel(const __grid_constant__ GatherParams p) {
+  constexpr int CH = R / 4;  // 16-byte chunks of one lane-word
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
-  __shared__ uint32_t tpos[1 << TPB_MAX];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int TP = 1 << p.tpb;
+  const int tid = threadIdx.x;
+  const int np = 1 << p.nbits;
+  const int w = blockIdx.y & 31, g = blockIdx.y >> 5;
   const uint32_t t = blockIdx.x;
-  const int g = blockIdx.y;
   uint32_t base = 0;
   for (int i = 0; i < p.nnb; ++i) base |= ((t >> i) & 1u) << p.nbit[i];
   const uint32_t hout = 1u << p.lgH_out;
-  if (tid < TP) {
-    uint32_t o = 0;
-    for (int m = 0; m < p.tpb; ++m) o |= ((uint32_t(tid) >> m) & 1u) << p.gbit[m];
-    tpos[tid] = o;
-  }
-  __syncthreads();
-  if (base >= hout) {
-    // all positions >= hout unless a tile bit reaches below hout's top; tile
-    // positions only add bits, so base >= hout means the whole tile is out.
-    return;
-  }
-  const uint4 *src = p.g + ((size_t(g) << p.lgH_in) * U4);
-  for (int idx = tid; idx < TP * U4; idx += NT) {
-    const int q = idx / U4, c = idx - q * U4;
-    cp_async16(smem + idx, src + size_t(base | tpos[q]) * U4 + c);
+  if (base >= hout) return;  // every position of the tile is >= hout
+  auto pos_of = [&](int q) {
+    uint32_t o = base;
+    for (int m = 0; m < p.nbits; ++m) o |= ((uint32_t(q) >> m) & 1u) << p.bits[m];
+    return o;
+  };
+  // stage lane-word w of every tile position (16-byte chunks, swizzled)
+  const uint4 *src = p.y + ((size_t(g) << p.lgH_in) * U4);
+  for (int idx = tid; idx < np * CH; idx += NT) {
+    const int q = idx / CH, c = idx - q * CH;
+    cp_async16(smem + q * CH + (c ^ ((q >> 1) & (CH - 1))),
+               src + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w, c));
   }
   cp_async_wait_all();
   __syncthreads();
-  uint4 *tb = p.t + ((size_t(g) << p.lgH_out) * U4);
-  for (int q = warp; q < TP; q += NWARP) {
-    const uint32_t pos = base | tpos[q];
+  auto ld = [&](int q, uint32_t (&v)[R]) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint4 x = smem[q * CH + (c ^ ((q >> 1) & (CH - 1)))];
+      v[4 * c + 0] = x.x;
+      v[4 * c + 1] = x.y;
+      v[4 * c + 2] = x.z;
+      v[4 * c + 3] = x.w;
+    }
+  };
+  uint4 *tout = p.t_out + ((size_t(g) << p.lgH_out) * U4);
+  const uint4 *tin = p.t_in ? p.t_in + ((size_t(g) << p.lgH_out) * U4) : nullptr;
+  for (int q = tid; q < np; q += NT) {
+    const uint32_t pos = pos_of(q);
     if (pos >= hout) continue;
     uint32_t acc[R];
-    if (p.acc_in) {
-      Blk<R>::load_g(tb + size_t(pos) * U4, lane, acc);
+    if (tin) {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const uint4 x = __ldg(tin + size_t(pos) * U4 + Blk<R>::chunk(w, c));
+        acc[4 * c + 0] = x.x;
+        acc[4 * c + 1] = x.y;
+        acc[4 * c + 2] = x.z;
+        acc[4 * c + 3] = x.w;
+      }
     } else {
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] = 0u;
     }
-    for (int m = 0; m < p.tpb; ++m) {
-      if ((q >> m) & 1) continue;
+    for (int m = 0; m < p.nbits; ++m) {
+      if (m == p.sb || ((q >> m) & 1)) continue;
       uint32_t x[R];
-      Blk<R>::load(smem + (q | (1 << m)) * U4, lane, x);
+      ld(q | (1 << m), x);
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= x[b];
     }
-    Blk<R>::store(tb + size_t(pos) * U4, lane, acc);
+    if (p.sb >= 0 && !((q >> p.sb) & 1)) {
+      uint32_t x[R], z[R], cz[R];
+      ld(q, x);
+      ld(q | (1 << p.sb), z);
+#pragma unroll
+      for (int b = 0; b < R; ++b) z[b] ^= x[b];
+      GF<R, POLY>::mul(cz, z, p.c);  // c is a kernel constant: uniform
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] ^= cz[b];
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      tout[size_t(pos) * U4 + Blk<R>::chunk(w, c)] =
+          make_uint4(acc[4 * c + 0], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
   }
 }
 
@@ -799,19 +844,19 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int R>
+template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s) {
-  const size_t smem = pass_smem_bytes(R, p.tpb, false);
+  const size_t smem = (size_t(1) << p.nbits) * R * 4;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gather_kernel<R>,
+    cudaError_t e = cudaFuncSetAttribute(gather_kernel<R, POLY>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(pass_smem_bytes(R, TPB_MAX, false)));
+                                         int((size_t(1) << GMAXB) * R * 4));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(1u << (p.lgH_in - p.tpb), ngroups);
-  gather_kernel<R><<<grid, NT, smem, s>>>(p);
+  dim3 grid(1u << (p.lgH_in - p.nbits), unsigned(ngroups) * 32u);
+  gather_kernel<R, POLY><<<grid, NT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -853,7 +898,7 @@ cudaError_t launch_count_bits(const uint32_t *bits, int64_t npatterns, int words
 
 template cudaError_t launch_pass<16, 0x1100Bu>(const PassParams &, int, cudaStream_t);
 template cudaError_t launch_pass<8, 0x11Du>(const PassParams &, int, cudaStream_t);
-template cudaError_t launch_gather<16>(const GatherParams &, int, cudaStream_t);
-template cudaError_t launch_gather<8>(const GatherParams &, int, cudaStream_t);
+template cudaError_t launch_gather<16, 0x1100Bu>(const GatherParams &, int, cudaStream_t);
+template cudaError_t launch_gather<8, 0x11Du>(const GatherParams &, int, cudaStream_t);
 
 }  // namespace lch

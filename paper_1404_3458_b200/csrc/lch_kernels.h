@@ -70,20 +70,30 @@ struct PassParams {
   RawIO raw_in, raw_out;
   const uint16_t *w_hat;
   uint32_t w_hat_off[17];
+  uint4 *gt_out;         // gather epilogue: partial derivative sums over the tile bits
+  int gt_lgH;
   int dbg;  // experiments only: 1 = skip global I/O, 2 = skip butterflies
 };
 
+// XOR-gather step of the formal derivative (derivative.py:60-70) over a set
+// of position bits, lanes over positions (no factor is involved, except the
+// optional constant-multiplied special bit):
+//   T[j] = T_in[j] + sum_{m != sb, bit m of j clear} y[j | 2^bits[m]]
+//                  + c * (y[j] + y[j | 2^bits[sb]])   (if sb >= 0, bit clear)
+// for j < 2^lgH_out.  One CTA per (tile, group, lane-word).
+constexpr int GMAXB = 11;
 struct GatherParams {
-  int tpb;
-  int gbit[TPB_MAX];
-  int lgH_in, lgH_out;   // g has 2^lgH_in positions, T has 2^lgH_out (prefix)
+  int nbits;
+  int bits[GMAXB];
+  int sb;                // index into bits[] of the special bit, or -1
+  uint32_t c;            // constant for the special bit
+  int lgH_in, lgH_out;
   int nnb;
   int nbit[16];
-  int acc_in;            // accumulate into existing T
-  const uint4 *g;
-  uint4 *t;
+  const uint4 *y;
+  const uint4 *t_in;     // may be null
+  uint4 *t_out;
 };
-
 struct FwhtParams {
   uint32_t *data;        // [nvec][2^lgn]
   int64_t nvec;
@@ -98,7 +108,7 @@ struct FwhtParams {
 
 template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s);
-template <int R>
+template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s);
 cudaError_t launch_fwht(const FwhtParams &p, cudaStream_t s);
 cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const uint16_t *exp,

@@ -307,7 +307,16 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
     std::memset(&p, 0, sizeof(p));
     std::vector<int> grp;
     const int room = GMAXB - (first && special >= 0 ? 1 : 0);
-    while (i < bits.size() && int(grp.size()) < room) grp.push_back(bits[i++]);
+    const bool has_tin = !first || t_in;
+    while (i < bits.size() && int(grp.size()) < room) {
+      // shared-memory budget: y tile (+ T_in at the tile's output positions)
+      int nlow = 0, nb = int(grp.size()) + 1 + (first && special >= 0 ? 1 : 0);
+      for (int b : grp) nlow += b < lgH_out;
+      nlow += bits[i] < lgH_out;
+      const size_t need = ((size_t(1) << nb) + (has_tin ? (size_t(1) << nlow) : 0)) * R * 4;
+      if (need > GATHER_SMEM_MAX) break;
+      grp.push_back(bits[i++]);
+    }
     p.sb = -1;
     if (first && special >= 0) {
       grp.push_back(special);

@@ -625,13 +625,21 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   }
 }
 
+constexpr int GNT = 512;  // gather threads per CTA
+
+// Tile bits are sorted, so the tile positions below 2^lgH_out (the outputs)
+// are exactly q < 2^nlow with nlow = #tile bits below lgH_out (base < 2^lgH_out).
 template <int R, uint32_t POLY>
-__global__ void __launch_bounds__(NT) gather_kernel(const __grid_constant__ GatherParams p) {
+__global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ GatherParams p) {
   constexpr int CH = R / 4;  // 16-byte chunks of one lane-word
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
   const int tid = threadIdx.x;
   const int np = 1 << p.nbits;
+  int nlow = 0;
+  while (nlow < p.nbits && p.bits[nlow] < p.lgH_out) ++nlow;
+  const int nout = 1 << nlow;
+  uint4 *ytile = smem, *ttile = smem + np * CH;
   const int w = blockIdx.y & 31, g = blockIdx.y >> 5;
   const uint32_t t = blockIdx.x;
   uint32_t base = 0;
@@ -643,19 +651,25 @@ __global__ void __launch_bounds__(NT) gather_kernel(const __grid_constant__ Gath
     for (int m = 0; m < p.nbits; ++m) o |= ((uint32_t(q) >> m) & 1u) << p.bits[m];
     return o;
   };
-  // stage lane-word w of every tile position (16-byte chunks, swizzled)
+  auto slot = [](int q, int c) { return q * CH + (c ^ ((q >> 1) & (CH - 1))); };
+  // stage lane-word w of every tile position (and of T_in at the outputs)
   const uint4 *src = p.y + ((size_t(g) << p.lgH_in) * U4);
-  for (int idx = tid; idx < np * CH; idx += NT) {
+  for (int idx = tid; idx < np * CH; idx += GNT) {
     const int q = idx / CH, c = idx - q * CH;
-    cp_async16(smem + q * CH + (c ^ ((q >> 1) & (CH - 1))),
-               src + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w, c));
+    cp_async16(ytile + slot(q, c), src + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w, c));
   }
+  const uint4 *tin = p.t_in ? p.t_in + ((size_t(g) << p.lgH_out) * U4) : nullptr;
+  if (tin)
+    for (int idx = tid; idx < nout * CH; idx += GNT) {
+      const int q = idx / CH, c = idx - q * CH;
+      cp_async16(ttile + slot(q, c), tin + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w, c));
+    }
   cp_async_wait_all();
   __syncthreads();
-  auto ld = [&](int q, uint32_t (&v)[R]) {
+  auto ld = [&](const uint4 *tile, int q, uint32_t (&v)[R]) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const uint4 x = smem[q * CH + (c ^ ((q >> 1) & (CH - 1)))];
+      const uint4 x = tile[slot(q, c)];
       v[4 * c + 0] = x.x;
       v[4 * c + 1] = x.y;
       v[4 * c + 2] = x.z;
@@ -663,20 +677,10 @@ __global__ void __launch_bounds__(NT) gather_kernel(const __grid_constant__ Gath
     }
   };
   uint4 *tout = p.t_out + ((size_t(g) << p.lgH_out) * U4);
-  const uint4 *tin = p.t_in ? p.t_in + ((size_t(g) << p.lgH_out) * U4) : nullptr;
-  for (int q = tid; q < np; q += NT) {
-    const uint32_t pos = pos_of(q);
-    if (pos >= hout) continue;
+  for (int q = tid; q < nout; q += GNT) {
     uint32_t acc[R];
     if (tin) {
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const uint4 x = __ldg(tin + size_t(pos) * U4 + Blk<R>::chunk(w, c));
-        acc[4 * c + 0] = x.x;
-        acc[4 * c + 1] = x.y;
-        acc[4 * c + 2] = x.z;
-        acc[4 * c + 3] = x.w;
-      }
+      ld(ttile, q, acc);
     } else {
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] = 0u;
@@ -684,25 +688,32 @@ __global__ void __launch_bounds__(NT) gather_kernel(const __grid_constant__ Gath
     for (int m = 0; m < p.nbits; ++m) {
       if (m == p.sb || ((q >> m) & 1)) continue;
       uint32_t x[R];
-      ld(q | (1 << m), x);
+      ld(ytile, q | (1 << m), x);
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= x[b];
     }
-    if (p.sb >= 0 && !((q >> p.sb) & 1)) {
+    if (p.sb >= 0) {  // q < nout has the special (top) bit clear
       uint32_t x[R], z[R], cz[R];
-      ld(q, x);
-      ld(q | (1 << p.sb), z);
+      ld(ytile, q, x);
+      ld(ytile, q | (1 << p.sb), z);
 #pragma unroll
       for (int b = 0; b < R; ++b) z[b] ^= x[b];
       GF<R, POLY>::mul(cz, z, p.c);  // c is a kernel constant: uniform
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= cz[b];
     }
+    const uint32_t pos = pos_of(q);
 #pragma unroll
     for (int c = 0; c < CH; ++c)
       tout[size_t(pos) * U4 + Blk<R>::chunk(w, c)] =
           make_uint4(acc[4 * c + 0], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
   }
+}
+
+size_t gather_smem_bytes(int R, const GatherParams &p) {
+  int nlow = 0;
+  while (nlow < p.nbits && p.bits[nlow] < p.lgH_out) ++nlow;
+  return ((size_t(1) << p.nbits) + (p.t_in ? (size_t(1) << nlow) : 0)) * R * 4;
 }
 
 // Walsh-Hadamard transform over Z_mod, bits [b0, b0 + tb) of each vector
@@ -846,17 +857,18 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
 
 template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s) {
-  const size_t smem = (size_t(1) << p.nbits) * R * 4;
+  const size_t smem = gather_smem_bytes(R, p);
+  if (smem > GATHER_SMEM_MAX) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gather_kernel<R, POLY>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int((size_t(1) << GMAXB) * R * 4));
+                                         int(GATHER_SMEM_MAX));
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid(1u << (p.lgH_in - p.nbits), unsigned(ngroups) * 32u);
-  gather_kernel<R, POLY><<<grid, NT, smem, s>>>(p);
+  gather_kernel<R, POLY><<<grid, GNT, smem, s>>>(p);
   return cudaGetLastError();
 }
 

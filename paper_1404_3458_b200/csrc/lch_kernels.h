@@ -82,6 +82,7 @@ struct PassParams {
 //                  + c * (y[j] + y[j | 2^bits[sb]])   (if sb >= 0, bit clear)
 // for j < 2^lgH_out.  One CTA per (tile, group, lane-word).
 constexpr int GMAXB = 11;
+constexpr size_t GATHER_SMEM_MAX = 200 * 1024;
 struct GatherParams {
   int nbits;
   int bits[GMAXB];
@@ -108,6 +109,7 @@ struct FwhtParams {
 
 template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s);
+size_t gather_smem_bytes(int R, const GatherParams &p);
 template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s);
 cudaError_t launch_fwht(const FwhtParams &p, cudaStream_t s);

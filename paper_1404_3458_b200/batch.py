@@ -111,6 +111,34 @@ class BatchCodec:
             encode_device(cp, self.bt, md, out[:, cp.k:])
         return self._back(messages, out)
 
+    def decode_patterns(self, received, erased_masks):
+        """Extension: one erasure pattern per row (rs.decode row by row, config 4b).
+
+        erased_masks: bool/uint8 array [stripes, n] (True = erased).  Rows may
+        erase 0..n-k positions; more raises TooManyErasuresError.
+        """
+        cp = self.cp
+        n, k = cp.n, cp.k
+        if received.shape[1] != n:
+            raise ValueError(f"received width {received.shape[1]} != n={n}")
+        torch = _lib.torch_mod()
+        rd = self._dev(received)
+        if _is_torch(erased_masks):
+            m = erased_masks.to("cuda").bool()
+        else:
+            m = torch.from_numpy(np.asarray(erased_masks).astype(bool)).to("cuda")
+        if m.shape != (rd.shape[0], n):
+            raise ValueError("erased_masks must be [stripes, n]")
+        from .gen import mask_to_bits
+        bits = mask_to_bits(m).contiguous()
+        counts = m.sum(dim=1).cpu().tolist()
+        if any(c > n - k for c in counts):
+            raise TooManyErasuresError(f"{max(counts)} erasures exceed repair capacity {n - k}")
+        out = torch.empty((rd.shape[0], k), dtype=torch.int16, device="cuda")
+        if rd.shape[0] > 0:
+            decode_device(cp, self.bt, rd, bits, out, counts)
+        return self._back(received, out)
+
     def decode(self, received, erased: set[int]):
         """Recover the (stripes x k) messages; erased columns are ignored (batch.py:126-153)."""
         cp = self.cp

@@ -357,8 +357,16 @@ uint32_t hs_of(const lch_ctx *c, int level, uint32_t shift) {
   return shift ? c->t.eval_w_hat(level, shift) : 0u;
 }
 
+struct DecodeEpi {
+  const uint16_t *rx = nullptr;
+  int64_t rx_stride = 0;
+  uint16_t *phi = nullptr;
+  uint16_t *pinv_log = nullptr;
+  uint32_t k = 0;
+};
+
 int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out, uint16_t *log_out,
-                 cudaStream_t s) {
+                 cudaStream_t s, const DecodeEpi *epi = nullptr) {
   const int r = c->t.r;
   const size_t n = size_t(1) << r;
   Scratch sc(s);
@@ -381,6 +389,15 @@ int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out
         p.exp = c->d_exp;
         p.loc_out = loc_out;
         p.log_out = log_out;
+        if (epi) {
+          p.bits_e = bits;
+          p.rx = epi->rx;
+          p.rx_stride = epi->rx_stride;
+          p.log = c->d_log;
+          p.phi = epi->phi;
+          p.pinv_log = epi->pinv_log;
+          p.k = epi->k;
+        }
       }
       LCH_TRY(cu(launch_fwht(p, s)));
       c->launches++;
@@ -612,6 +629,103 @@ int lch_encode(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *par
   });
 }
 
+// Decode with one erasure pattern per codeword (rs.decode row by row):
+// batched locator whose epilogue writes phi = rx * Pi_bar (rs.py:130-134) and
+// -log Pi' (rs.py:141-148); the shared transform pipeline without the
+// per-position scaling; the output epilogue divides erased symbols by Pi'.
+static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in,
+                               const uint32_t *bits, uint16_t *out, int64_t stride_out,
+                               int64_t batch, int lg_k, const int64_t *host_counts,
+                               cudaStream_t s) {
+  const int r = c->t.r;
+  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k;
+  const int words = int(n / 32);
+  {
+    std::vector<int64_t> counts(size_t(batch), 0);
+    if (host_counts) {
+      std::memcpy(counts.data(), host_counts, sizeof(int64_t) * size_t(batch));
+    } else {
+      Scratch sc(s);
+      int64_t *dc = nullptr;
+      LCH_TRY(sc.alloc(dc, size_t(batch)));
+      LCH_TRY(cu(launch_count_bits(bits, batch, words, dc, s)));
+      c->launches++;
+      LCH_TRY(cu(cudaMemcpyAsync(counts.data(), dc, sizeof(int64_t) * size_t(batch),
+                                 cudaMemcpyDeviceToHost, s)));
+      LCH_TRY(cu(cudaStreamSynchronize(s)));
+    }
+    for (int64_t cnt : counts)
+      if (cnt > n - k) return LCH_ETOOMANY;  // rs.py:121-123
+  }
+  if (c->max_lg_h < r) return LCH_EINVAL;
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    Scratch sc(s);
+    const int lgk_out = std::max(lg_k, 1);
+    uint16_t *phi = nullptr, *pinv_log = nullptr;
+    LCH_TRY(sc.alloc(phi, size_t(batch) * size_t(n)));
+    LCH_TRY(sc.alloc(pinv_log, size_t(batch) * size_t(std::max<int64_t>(k, 2))));
+    DecodeEpi epi;
+    epi.rx = rx;
+    epi.rx_stride = stride_in;
+    epi.phi = phi;
+    epi.pinv_log = pinv_log;
+    epi.k = uint32_t(std::max<int64_t>(k, 2));  // bound and row stride of pinv_log
+    // phi is written with the received words' row stride
+    if (stride_in != n) {
+      uint16_t *phi2 = nullptr;
+      LCH_TRY(sc.alloc(phi2, size_t(batch) * size_t(stride_in)));
+      epi.phi = phi2;
+    }
+    LCH_TRY(locator_impl(c, bits, batch, nullptr, nullptr, s, &epi));
+    uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
+    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, r) / 16));
+    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, lgk_out) / 16));
+    LCH_TRY(sc.alloc(t1, bs_bytes(R, batch, lgk_out) / 16));
+    RawIO in_io = make_raw(epi.phi, stride_in);
+    std::vector<LOp> a;
+    for (int i = 0; i + 1 < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
+    a.push_back({OP_SCALE, 0, 0, c->d_b_lo});
+    auto plan_a = plan_passes(a, r, true, false);
+    LCH_TRY((run_plan<R, P>(c, plan_a, r, batch, &in_io, nullptr, nullptr, x, s, t1, lgk_out)));
+    std::vector<int> rest;
+    for (int b = 0; b + 1 < r; ++b)
+      if (std::find(plan_a.back().bits.begin(), plan_a.back().bits.end(), b) == plan_a.back().bits.end())
+        rest.push_back(b);
+    rest.push_back(r - 1);
+    LCH_TRY((run_gather<R, P>(c, x, t, r, lgk_out, batch, rest, r - 1, c->t.w_prime[r - 1], t1, s)));
+    std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
+    for (int i = lg_k - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
+    const int lgo = std::max(lg_k, 1);
+    uint16_t *dst = out;
+    int64_t dst_stride = stride_out;
+    uint16_t *tmp = nullptr;
+    if (lg_k == 0) {  // 2-column scratch output, column 0 copied below
+      LCH_TRY(sc.alloc(tmp, size_t(batch) * 8));
+      dst = tmp;
+      dst_stride = 8;
+    }
+    RawIO out_io = make_raw(dst, dst_stride);
+    out_io.merge_src = rx;
+    out_io.merge_stride = stride_in;
+    out_io.merge_bits = bits;
+    out_io.bits_stride = words;
+    out_io.pinv_log = pinv_log;
+    out_io.pinv_stride = std::max<int64_t>(k, 2);
+    out_io.log_tab = c->d_log;
+    out_io.exp_tab = c->d_exp;
+    out_io.mord = c->t.m;
+    out_io.vec = out_io.vec && lg_k > 0 && (reinterpret_cast<uintptr_t>(rx) % 16 == 0) &&
+                 (stride_in % 8 == 0);
+    LCH_TRY((run_plan<R, P>(c, plan_passes(b, lgo, false, true), lgo, batch, nullptr, t, &out_io, t, s)));
+    if (lg_k == 0)
+      return cu(cudaMemcpy2DAsync(out, size_t(stride_out) * 2, tmp, 16, 2, size_t(batch),
+                                  cudaMemcpyDeviceToDevice, s));
+    return LCH_OK;
+  });
+}
+
 int lch_decode(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t *bits, int shared,
                uint16_t *out, int64_t stride_out, int64_t batch, int lg_k, int64_t packet_len,
                const int64_t *host_counts, void *stream) {
@@ -623,8 +737,9 @@ int lch_decode(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t
   if (stride_in < n || stride_out < k) return LCH_EINVAL;
   LCH_TRY(ensure_device(c));
   if (batch == 0) return LCH_OK;
-  if (!shared) return LCH_EUNSUPPORTED;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!shared) return decode_per_codeword(c, rx, stride_in, bits, out, stride_out, batch, lg_k,
+                                          host_counts, s);
   int64_t count = 0;
   if (host_counts) {
     count = host_counts[0];

@@ -285,11 +285,23 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
                              rs[stage_idx(r, 4 * c + 2)], rs[stage_idx(r, 4 * c + 3)]);
       const uint32_t pos0 = base + 8 * c;
       if (io.merge_src) {
-        const uint32_t eb = (io.merge_bits[pos0 >> 5] >> (pos0 & 31)) & 0xFFu;
+        const uint32_t *mb = io.merge_bits + b * io.bits_stride;
+        const uint32_t eb = (mb[pos0 >> 5] >> (pos0 & 31)) & 0xFFu;
+        uint32_t *vv = &val.x;
+        if (io.pinv_log && eb) {
+          const uint16_t *pl = io.pinv_log + b * io.pinv_stride + pos0;
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            if (!((eb >> h) & 1u)) continue;
+            const uint32_t sh = 16 * (h & 1);
+            const uint32_t x = (vv[h >> 1] >> sh) & 0xFFFFu;
+            const uint32_t y = x ? io.exp_tab[(uint32_t(__ldg(io.log_tab + x)) + __ldg(pl + h)) % io.mord] : 0u;
+            vv[h >> 1] = (vv[h >> 1] & ~(0xFFFFu << sh)) | (y << sh);
+          }
+        }
         if (eb != 0xFFu) {
           const uint4 src =
               __ldg(reinterpret_cast<const uint4 *>(io.merge_src + b * io.merge_stride + pos0));
-          uint32_t *vv = &val.x;
           const uint32_t *ss = &src.x;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
@@ -311,8 +323,13 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
       for (int h = 0; h < 2; ++h) {
         const uint32_t pos = base + 2 * cw + h;
         uint16_t v = uint16_t(h ? (w >> 16) : (w & 0xFFFFu));
-        if (io.merge_src && !((io.merge_bits[pos >> 5] >> (pos & 31)) & 1u))
-          v = io.merge_src[b * io.merge_stride + pos];
+        if (io.merge_src) {
+          const bool erased = (io.merge_bits[b * io.bits_stride + (pos >> 5)] >> (pos & 31)) & 1u;
+          if (!erased)
+            v = io.merge_src[b * io.merge_stride + pos];
+          else if (io.pinv_log && v)
+            v = io.exp_tab[(uint32_t(io.log_tab[v]) + io.pinv_log[b * io.pinv_stride + pos]) % io.mord];
+        }
         io.ptr[b * io.row_stride + pos] = v;
       }
     }
@@ -752,7 +769,15 @@ __global__ void fwht_kernel(const __grid_constant__ FwhtParams p) {
   }
   x = s[q];
   if (p.post_mul) x = uint32_t((uint64_t(x) * p.post_mul[pos]) % mod);
-  if (p.exp) {
+  if (p.phi) {
+    // x = log of the locator value at pos (Pi_bar if surviving, Pi' if erased)
+    const bool erased = (p.bits_e[size_t(vec) * words + (pos >> 5)] >> (pos & 31)) & 1u;
+    const uint16_t r = p.rx[size_t(vec) * p.rx_stride + pos];
+    p.phi[size_t(vec) * p.rx_stride + pos] =
+        (erased || r == 0) ? uint16_t(0) : p.exp[(uint32_t(p.log[r]) + x) % p.mod];
+    if (pos < p.k)
+      p.pinv_log[size_t(vec) * p.k + pos] = erased ? uint16_t((p.mod - x) % p.mod) : uint16_t(0);
+  } else if (p.exp) {
     const uint16_t val = p.exp[x];
     if (p.loc_out) p.loc_out[idx] = val;
     if (p.log_out) p.log_out[idx] = uint16_t(x);

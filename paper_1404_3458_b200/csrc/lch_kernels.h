@@ -40,14 +40,25 @@ struct PassRound {
 // Raw uint16 batch: element (b, j) at ptr[b * row_stride + j].
 // Decode epilogue: if merge_src, out(b, j) = erased(j) ? computed : merge_src(b, j)
 // with erased(j) = bit j of merge_bits.
+// Raw uint16 batch: element (b, j) at ptr[b * row_stride + j].
+// Decode epilogue (merge_src != null): out(b, j) = erased(b, j) ? computed' :
+// merge_src(b, j), with erased(b, j) = bit j of merge_bits + b * bits_stride
+// (bits_stride = 0: one shared pattern) and computed' = computed, or, with
+// per-codeword patterns (pinv_log != null), computed * alpha^pinv_log(b, j)
+// (division by Pi'(j), rs.py:141-148) through the log/exp tables.
 struct RawIO {
   uint16_t *ptr;
   int64_t row_stride;
   const uint16_t *merge_src;
   int64_t merge_stride;
   const uint32_t *merge_bits;
+  int64_t bits_stride;      // words between consecutive rows' bitmasks (0 = shared)
+  const uint16_t *pinv_log; // [batch][pinv_stride] or null
+  int64_t pinv_stride;
+  const uint16_t *log_tab, *exp_tab;
+  uint32_t mord;            // 2^r - 1
   int vec;  // 16-byte vector accesses allowed
-  int al4;  // 4-byte aligned rows (asynchronous 32-bit staging copies)
+  int al4;  // 4-byte aligned rows
 };
 
 struct PassParams {
@@ -101,10 +112,19 @@ struct FwhtParams {
   int lgn, b0, tb;       // this pass covers bits [b0, b0 + tb)
   uint32_t mod;
   const uint32_t *bits;  // indicator input (bitmask) when non-null
+  const uint32_t *bits_e;  // erasure bitmask for the decode epilogue
   const uint32_t *post_mul;  // multiply by post_mul[j] mod after the pass
   // epilogue (locator): loc = exp[x], log = x
   const uint16_t *exp;
   uint16_t *loc_out, *log_out;
+  // per-codeword decode epilogue (rs.py:130-134, 141-148): phi = rx * Pi_bar
+  // on survivors (0 on erasures) and pinv_log = -log Pi' on erased j < k
+  const uint16_t *rx;
+  int64_t rx_stride;
+  const uint16_t *log;
+  uint16_t *phi;
+  uint16_t *pinv_log;
+  uint32_t k;
 };
 
 template <int R, uint32_t POLY>

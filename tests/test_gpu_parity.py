@@ -275,3 +275,61 @@ def test_fwht_vs_oracle(lch):
         np.testing.assert_array_equal(lch.fwht(list(v), mod), O.fwht(v, mod))
     assert lch.fwht([7, 3], 255) == [10, 4]
     assert lch.fwht([3, 7], 255) == [10, 251]
+
+
+def test_decode_per_codeword_r8_cfg1_golden(lch, bt8):
+    # config 1: 64 codewords, 128 erasures drawn per codeword (rs.decode row by row)
+    codec = lch.BatchCodec(lch.CodeParams(8, 128), bt8)
+    masks = G8["cfg1_mask"].astype(bool)
+    rx = np.where(masks, 0, G8["cfg1_cw"]).astype(np.uint16)
+    np.testing.assert_array_equal(codec.decode_patterns(rx, masks), G8["cfg1_msg"])
+    junk = np.stack([O.gen_symbols(1404345801 ^ 0x5A5A, 8, row, 1, 256)[0] for row in range(64)])
+    np.testing.assert_array_equal(codec.decode_patterns(junk, masks), G8["cfg1_junk_dec"])
+
+
+@pytest.mark.parametrize("k", [1, 4, 64])
+def test_decode_per_codeword_r8_mixed_counts(lch, bt8, orc8, k):
+    codec = lch.BatchCodec(lch.CodeParams(8, k), bt8)
+    B = 1100
+    junk = O.gen_symbols(31 + k, 8, 0, B, 256)
+    counts = [(7 * i) % (256 - k + 1) for i in range(B)]  # includes empty patterns
+    masks = np.stack([O.gen_erasures(500 + i, 256, counts[i], i, 1)[0] for i in range(B)])
+    out = codec.decode_patterns(junk, masks)
+    for r in list(range(0, B, 97)) + [B - 1]:
+        if counts[r] == 0:
+            np.testing.assert_array_equal(out[r], junk[r, :k])
+        else:
+            np.testing.assert_array_equal(out[r], orc8.decode(k, junk[r], masks[r]), err_msg=f"row {r}")
+    with pytest.raises(lch.TooManyErasuresError):
+        bad = masks.copy()
+        bad[3] = 0
+        bad[3, : 256 - k + 1] = 1
+        codec.decode_patterns(junk, bad)
+
+
+def test_decode_per_codeword_r16_vs_oracle(lch, bt16, orc16):
+    import torch
+    from paper_1404_3458_b200 import gen as G
+    from paper_1404_3458_b200.rs import decode_device, encode_device
+    n, k, B = 1 << 16, 1 << 15, 1030
+    cp = lch.CodeParams(16, k)
+    msg = gen(bt16, 1404345803, 0, B, k)
+    cw = torch.empty((B, n), dtype=torch.int16, device="cuda")
+    cw[:, :k].copy_(msg)
+    encode_device(cp, bt16, msg, cw[:, k:])
+    emask = G.erasure_masks(bt16.ctx, 1404345804, n, n - k, 0, B)  # per-codeword patterns
+    bits = G.mask_to_bits(emask).contiguous()
+    rx = cw.masked_fill(emask, 0)
+    out = torch.empty((B, k), dtype=torch.int16, device="cuda")
+    decode_device(cp, bt16, rx, bits, out, [n - k] * B)
+    np.testing.assert_array_equal(host(out), host(msg))
+    # pattern generator matches the oracle's (rows 0 and 7)
+    for r in (0, 7):
+        np.testing.assert_array_equal(emask[r].cpu().numpy().astype(np.uint8),
+                                      O.gen_erasures(1404345804, n, n - k, r, 1)[0])
+    junk = gen(bt16, 99, 0, 3, n)
+    jout = torch.empty((3, k), dtype=torch.int16, device="cuda")
+    decode_device(cp, bt16, junk, bits[:3].contiguous(), jout, [n - k] * 3)
+    jh, mh = host(junk), emask[:3].cpu().numpy().astype(np.uint8)
+    for r in range(3):
+        np.testing.assert_array_equal(host(jout)[r], orc16.decode(k, jh[r], mh[r]), err_msg=f"row {r}")

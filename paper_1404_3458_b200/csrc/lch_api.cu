@@ -103,6 +103,7 @@ struct LOp {
   int level;
   uint32_t hs;
   const uint16_t *table;
+  int64_t tab_stride = 0;  // per stripe-group table rows (packet layout)
 };
 
 struct Plan {
@@ -234,10 +235,15 @@ void fill_bits(const std::vector<int> &bits, int lgH, int *gbit, int &nnb, int *
     if (std::find(bits.begin(), bits.end(), b) == bits.end()) nbit[nnb++] = b;
 }
 
-RawIO make_raw(uint16_t *ptr, int64_t stride) {
+RawIO make_raw(uint16_t *ptr, int64_t stride, int64_t pkt = 0, int64_t npos = 0,
+               int64_t pos_lo = 0, int64_t pos_hi = int64_t(1) << 40) {
   RawIO io{};
   io.ptr = ptr;
   io.row_stride = stride;
+  io.pkt = pkt;
+  io.npos = npos;
+  io.pos_lo = pos_lo;
+  io.pos_hi = pos_hi;
   io.vec = (reinterpret_cast<uintptr_t>(ptr) % 16 == 0) && (stride % 8 == 0);
   io.al4 = (reinterpret_cast<uintptr_t>(ptr) % 4 == 0) && (stride % 2 == 0);
   return io;
@@ -246,7 +252,7 @@ RawIO make_raw(uint16_t *ptr, int64_t stride) {
 template <int R, uint32_t POLY>
 int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, const RawIO *raw_in,
              const uint4 *bs_in, const RawIO *raw_out, uint4 *work, cudaStream_t s,
-             uint4 *gt_out = nullptr, int gt_lgH = 0) {
+             uint4 *gt_out = nullptr, int gt_lgH = 0, int64_t pkt = 0) {
   const int ngroups = int((batch + GROUP - 1) / GROUP);
   for (size_t i = 0; i < plan.size(); ++i) {
     const Plan &pl = plan[i];
@@ -255,13 +261,16 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     LCH_TRY(build_rounds(pl, p));
     p.npre = int(pl.pre.size());
     p.npost = int(pl.post.size());
-    for (int o = 0; o < p.npre; ++o) p.pre[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.pre[o].table};
-    for (int o = 0; o < p.npost; ++o) p.post[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.post[o].table};
+    for (int o = 0; o < p.npre; ++o)
+      p.pre[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.pre[o].table, pl.pre[o].tab_stride};
+    for (int o = 0; o < p.npost; ++o)
+      p.post[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.post[o].table, pl.post[o].tab_stride};
     p.tpb = int(pl.bits.size());
     p.lgH = lgH;
     fill_bits(pl.bits, lgH, p.gbit, p.nnb, p.nbit);
     p.batch = batch;
     p.ngroups = ngroups;
+    p.pkt = pkt;
     const bool first = i == 0, last = i + 1 == plan.size();
     p.in_mode = (first && raw_in) ? IO_RAW : IO_BS;
     p.out_mode = (last && raw_out) ? IO_RAW : IO_BS;

@@ -160,11 +160,14 @@ __host__ __device__ constexpr int stage_offset_u4() {
   return bs_offset_u4<R>() + (1 << TPB_MAX) * 8 * R;
 }
 
-// Issue the loads of a tile: BS input asynchronously (cp.async, no wait),
-// raw input synchronously through registers into the staging layout.
-// BS input: thread 0 issues one 2 KB (R = 16) bulk copy per position block,
-// completing on `bar` (the caller waits on it).  The caller guarantees every
-// thread finished its shared-memory accesses to the tile (barrier) before.
+// Raw element address (see RawIO); b = batch index, j = position.
+__device__ __forceinline__ const uint16_t *raw_addr(const RawIO &io, int64_t b, int64_t j) {
+  if (io.pkt) return io.ptr + ((b / io.pkt) * io.npos + (j - io.pos_lo)) * io.pkt + b % io.pkt;
+  return io.ptr + b * io.row_stride + (j - io.pos_lo);
+}
+
+// Issue the loads of a tile: BS input asynchronously (TMA bulk copies, see
+// below), raw input synchronously through registers into the staging layout.
 template <int R>
 __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, const uint32_t *tpos,
                                            int g, uint32_t base, int TP, uint64_t *bar) {
@@ -193,27 +196,45 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
   const int WPR = TP >> 1;
   const int64_t row0 = int64_t(g) * GROUP;
   const RawIO &io = p.raw_in;
-  if (io.vec && TP >= 8) {
+  const bool inwin = int64_t(base) >= io.pos_lo && int64_t(base) + TP <= io.pos_hi;
+  if (io.pkt && inwin) {
+    // packet-major: 1024 consecutive symbols per position; a thread takes 8
+    // rows of one word column (positions 2cw, 2cw+1) and interleaves them
+    for (int idx = threadIdx.x; idx < WPR * (GROUP / 8); idx += NT) {
+      const int cw = idx / (GROUP / 8), r8 = idx - cw * (GROUP / 8);
+      const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(raw_addr(io, row0 + 8 * r8, base + 2 * cw)));
+      const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(raw_addr(io, row0 + 8 * r8, base + 2 * cw + 1)));
+      uint4 lo, hi;
+      lo.x = __byte_perm(a.x, b.x, 0x5410); lo.y = __byte_perm(a.x, b.x, 0x7632);
+      lo.z = __byte_perm(a.y, b.y, 0x5410); lo.w = __byte_perm(a.y, b.y, 0x7632);
+      hi.x = __byte_perm(a.z, b.z, 0x5410); hi.y = __byte_perm(a.z, b.z, 0x7632);
+      hi.z = __byte_perm(a.w, b.w, 0x5410); hi.w = __byte_perm(a.w, b.w, 0x7632);
+      uint4 *dst = reinterpret_cast<uint4 *>(rs + stage_idx(8 * r8, cw));
+      dst[0] = lo;
+      dst[1] = hi;
+    }
+  } else if (!io.pkt && io.vec && TP >= 8 && inwin) {
     const int lcpr = p.tpb - 3;
     for (int idx = threadIdx.x; idx < (GROUP << lcpr); idx += NT) {
       const int r = idx >> lcpr, c = idx & ((1 << lcpr) - 1);
       const int64_t b = row0 + r;
       uint4 val = make_uint4(0u, 0u, 0u, 0u);
-      if (b < p.batch)
-        val = __ldcs(reinterpret_cast<const uint4 *>(io.ptr + b * io.row_stride + base) + c);
+      if (b < p.batch) val = __ldcs(reinterpret_cast<const uint4 *>(raw_addr(io, b, base)) + c);
       rs[stage_idx(r, 4 * c + 0)] = val.x;
       rs[stage_idx(r, 4 * c + 1)] = val.y;
       rs[stage_idx(r, 4 * c + 2)] = val.z;
       rs[stage_idx(r, 4 * c + 3)] = val.w;
     }
-  } else {  // small tiles / unaligned rows: 2 x 16-bit loads per word
+  } else {  // small / partial tiles, unaligned rows: element loads
     for (int idx = threadIdx.x; idx < GROUP * WPR; idx += NT) {
       const int r = idx / WPR, cw = idx - r * WPR;
       const int64_t b = row0 + r;
       uint32_t w = 0;
       if (b < p.batch) {
-        const uint16_t *src = io.ptr + b * io.row_stride + base + 2 * cw;
-        w = uint32_t(src[0]) | (uint32_t(src[1]) << 16);
+        const int64_t j = int64_t(base) + 2 * cw;
+        const uint32_t lo = (j >= io.pos_lo && j < io.pos_hi) ? *raw_addr(io, b, j) : 0u;
+        const uint32_t hi = (j + 1 >= io.pos_lo && j + 1 < io.pos_hi) ? *raw_addr(io, b, j + 1) : 0u;
+        w = lo | (hi << 16);
       }
       rs[stage_idx(r, cw)] = w;
     }
@@ -275,7 +296,33 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
     for (int L = 0; L < 32; ++L) rs[stage_idx(32 * L + lane, cw)] = a[L];
   }
   __syncthreads();
-  if (io.vec && TP >= 8) {
+  const bool inwin = int64_t(base) >= io.pos_lo && int64_t(base) + TP <= io.pos_hi;
+  auto erased_at = [&](int64_t b, int64_t j) -> bool {
+    const int64_t row = io.pkt ? b / io.pkt : b;
+    return (io.merge_bits[row * io.bits_stride + (j >> 5)] >> (j & 31)) & 1u;
+  };
+  if (io.pkt && inwin) {
+    for (int idx = tid; idx < WPR * (GROUP / 8); idx += NT) {
+      const int cw = idx / (GROUP / 8), r8 = idx - cw * (GROUP / 8);
+      const uint4 *srcw = reinterpret_cast<const uint4 *>(rs + stage_idx(8 * r8, cw));
+      const uint4 lo = srcw[0], hi = srcw[1];
+      uint4 a, b;  // positions 2cw (low halves) and 2cw + 1 (high halves), 8 symbols each
+      a.x = __byte_perm(lo.x, lo.y, 0x5410); b.x = __byte_perm(lo.x, lo.y, 0x7632);
+      a.y = __byte_perm(lo.z, lo.w, 0x5410); b.y = __byte_perm(lo.z, lo.w, 0x7632);
+      a.z = __byte_perm(hi.x, hi.y, 0x5410); b.z = __byte_perm(hi.x, hi.y, 0x7632);
+      a.w = __byte_perm(hi.z, hi.w, 0x5410); b.w = __byte_perm(hi.z, hi.w, 0x7632);
+      const int64_t bb = row0 + 8 * r8;
+      const int64_t j0 = int64_t(base) + 2 * cw;
+      if (io.merge_src) {  // packet erasures: the 8 symbols share the flag
+        // packet layout: merge_stride = positions per stripe group of merge_src
+        const uint16_t *ms = io.merge_src + (bb / io.pkt) * io.merge_stride * io.pkt + bb % io.pkt;
+        if (!erased_at(bb, j0)) a = __ldg(reinterpret_cast<const uint4 *>(ms + j0 * io.pkt));
+        if (!erased_at(bb, j0 + 1)) b = __ldg(reinterpret_cast<const uint4 *>(ms + (j0 + 1) * io.pkt));
+      }
+      *reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, bb, j0))) = a;
+      *reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, bb, j0 + 1))) = b;
+    }
+  } else if (!io.pkt && io.vec && TP >= 8 && inwin) {
     const int lcpr = p.tpb - 3;
     for (int idx = tid; idx < (GROUP << lcpr); idx += NT) {
       const int r = idx >> lcpr, c = idx & ((1 << lcpr) - 1);
@@ -311,7 +358,7 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
           }
         }
       }
-      *(reinterpret_cast<uint4 *>(io.ptr + b * io.row_stride + base) + c) = val;
+      reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, b, base)))[c] = val;
     }
   } else {
     for (int idx = tid; idx < GROUP * WPR; idx += NT) {
@@ -321,16 +368,18 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
       const uint32_t w = rs[stage_idx(r, cw)];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint32_t pos = base + 2 * cw + h;
+        const int64_t pos = int64_t(base) + 2 * cw + h;
+        if (pos < io.pos_lo || pos >= io.pos_hi) continue;
         uint16_t v = uint16_t(h ? (w >> 16) : (w & 0xFFFFu));
         if (io.merge_src) {
-          const bool erased = (io.merge_bits[b * io.bits_stride + (pos >> 5)] >> (pos & 31)) & 1u;
-          if (!erased)
-            v = io.merge_src[b * io.merge_stride + pos];
-          else if (io.pinv_log && v)
+          if (!erased_at(b, pos)) {
+            v = io.pkt ? io.merge_src[((b / io.pkt) * io.merge_stride + pos) * io.pkt + b % io.pkt]
+                       : io.merge_src[b * io.merge_stride + pos];
+          } else if (io.pinv_log && v) {
             v = io.exp_tab[(uint32_t(io.log_tab[v]) + io.pinv_log[b * io.pinv_stride + pos]) % io.mord];
+          }
         }
-        io.ptr[b * io.row_stride + pos] = v;
+        *const_cast<uint16_t *>(raw_addr(io, b, pos)) = v;
       }
     }
   }
@@ -340,7 +389,8 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
 
 template <int R, uint32_t POLY>
 __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *smem,
-                                            const uint32_t *tpos, uint32_t base, int TP) {
+                                            const uint32_t *tpos, uint32_t base, int TP,
+                                            int64_t trow) {
   using F = GF<R, POLY>;
   constexpr int U4 = Blk<R>::U4;
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
@@ -348,7 +398,8 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
     uint32_t v[R];
     Blk<R>::load(smem + q * U4, lane, v);
     for (int o = 0; o < nops; ++o) {
-      const uint32_t f = __shfl_sync(0xffffffffu, uint32_t(__ldg(ops[o].table + (base | tpos[q]))), 0);
+      const uint32_t f = __shfl_sync(
+          0xffffffffu, uint32_t(__ldg(ops[o].table + trow * ops[o].tab_stride + (base | tpos[q]))), 0);
       uint32_t acc[R];
       if (f) {
         F::mul(acc, v, f);
@@ -473,7 +524,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       __syncthreads();
     }
     if (p.npre) {
-      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP);
+      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
       __syncthreads();
     }
     for (int rd = 0; rd < p.nrounds; ++rd) {
@@ -590,7 +641,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     }
     if (!reg_path) {
       if (p.npost) {
-        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP);
+        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
         __syncthreads();
       }
       if (p.gt_out) {

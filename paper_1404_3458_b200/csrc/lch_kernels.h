@@ -25,6 +25,7 @@ struct PassOp {
   int level;              // global butterfly level i
   uint32_t hs;            // W^_i(shift) (0 for shift 0)
   const uint16_t *table;  // per-position factors (SCALE), indexed by position
+  int64_t tab_stride;     // SCALE: + (stripe group) * tab_stride (0: one row for all)
 };
 
 // A round: every thread holds the 4 positions spanned by tile bits m0, m1
@@ -49,6 +50,12 @@ struct PassRound {
 struct RawIO {
   uint16_t *ptr;
   int64_t row_stride;
+  // packet-major layout (pkt > 0): element (b, j) at
+  // ptr[((b / pkt) * npos + (j - pos_lo)) * pkt + b % pkt]; row-major
+  // otherwise.  Only positions j in [pos_lo, pos_hi) exist in the buffer
+  // (loads outside read 0, stores outside are dropped).
+  int64_t pkt, npos;
+  int64_t pos_lo, pos_hi;
   const uint16_t *merge_src;
   int64_t merge_stride;
   const uint32_t *merge_bits;
@@ -75,6 +82,7 @@ struct PassParams {
   int nbit[16];          // non-tile bit i -> global position bit
   int64_t batch;
   int ngroups;           // 1024-lane batch groups
+  int64_t pkt;           // stripe-group size in batch lanes (table rows), 0 = none
   int in_mode, out_mode;
   const uint4 *bs_in;    // BS buffers: block (g, pos) = 32*R words at ((g << lgH) + pos) * 8R uint4
   uint4 *bs_out;

@@ -13,7 +13,11 @@
  *  - Row-major batches: element (b, j) at ptr[b * row_stride + j]
  *    (row_stride in elements, >= the row length).  Packet-major batches
  *    (packet_len P > 0): element (g, j, s) of stripe group g, position j,
- *    packet symbol s at ptr[(g * n_pos + j) * P + s]; batch = groups * P.
+ *    packet symbol s at ptr[(g * n_pos + j) * P + s]; batch = groups * P,
+ *    P a multiple of 1024, pointers 16-byte aligned, and the stride
+ *    arguments give n_pos (positions per stripe group).  Lane g * P + s of a
+ *    stripe group is an ordinary codeword (shard j = symbol j of every
+ *    stripe, shardfile.py:16-20,129-140).
  *  - All data pointers are DEVICE pointers unless the name says host_.
  *    `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
  *    asynchronous with respect to the host unless stated otherwise.
@@ -110,6 +114,7 @@ int lch_encode(lch_ctx *ctx, const uint16_t *msg, int64_t row_stride_in,
  * (shared = 0); out: [batch][k] (row_stride_out).  Returns LCH_ETOOMANY when a
  * pattern erases more than n - k positions; an empty pattern is a copy.
  * Replaces rs.decode (rs.py:99-149) and BatchCodec.decode (batch.py:126-153).
+ * Packet layout: see lch_decode_k (shared = 0 means one pattern per group).
  * host_counts (optional): per-pattern erasure counts if the caller already
  * knows them (skips a device->host read). */
 int lch_decode(lch_ctx *ctx, const uint16_t *rx, int64_t row_stride_in,
@@ -117,10 +122,42 @@ int lch_decode(lch_ctx *ctx, const uint16_t *rx, int64_t row_stride_in,
                int64_t row_stride_out, int64_t batch, int lg_k, int64_t packet_len,
                const int64_t *host_counts, void *stream);
 
+/* General-k systematic RS(2^r, k) encode, 1 <= k <= 2^r.
+ * The codeword is the evaluation at omega_0..omega_(n-1) of the unique
+ * polynomial of degree < k through the message at omega_0..omega_(k-1)
+ * (novel-basis interpolation).  For power-of-two k this is lch_encode
+ * (rs.encode, rs.py:85-96); otherwise the parity is computed by erasure-
+ * decoding E = [k, n) with the reference's decode algorithm (rs.py:125-148):
+ * locator of E, Phi = msg * Pi_bar, n-point inverse, derivative, n-point
+ * forward, division by Pi' on [k, n).  Layouts as lch_encode; in packet
+ * layout the strides count positions per stripe group. */
+int lch_encode_k(lch_ctx *ctx, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
+                 int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len,
+                 void *stream);
+
+/* General-k erasure decode (rs.decode, rs.py:99-149 with the power-of-two
+ * restriction of rs.py:43-44 lifted): recovers positions [0, k) from any
+ * <= n - k erasures.  Row layout: shared = 1 (one pattern) or 0 (one per
+ * row; k <= n/2).  Packet layout: shared = 1 (one pattern) or 0 (one pattern
+ * per stripe group, erasure_bits [batch / packet_len][2^r / 32]). */
+int lch_decode_k(lch_ctx *ctx, const uint16_t *rx, int64_t stride_in,
+                 const uint32_t *erasure_bits, int shared, uint16_t *out, int64_t stride_out,
+                 int64_t batch, int64_t k, int64_t packet_len, const int64_t *host_counts,
+                 void *stream);
+
+/* Device scratch budget per call (bytes, default 4 GiB): batches whose
+ * bit-sliced intermediates exceed it are processed in lane chunks. */
+int lch_set_scratch_limit(lch_ctx *ctx, uint64_t bytes);
+
 /* Seeded counter-based inputs (oracle/lch_oracle.c orc_key):
  * out[b][j] = key(seed, cw0 + b, j) & (2^r - 1), row-major with row_stride. */
 int lch_gen_symbols(lch_ctx *ctx, uint64_t seed, uint64_t cw0, int64_t batch,
                     int64_t len, uint16_t *out, int64_t row_stride, void *stream);
+/* Packet-major seeded inputs: lane b = g * packet_len + s holds codeword
+ * cw0 + b, so out[(g * n_pos + j) * packet_len + s] = key(seed, cw0 + b, j)
+ * & (2^r - 1) for j < len (batch = groups * packet_len). */
+int lch_gen_packets(lch_ctx *ctx, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
+                    uint16_t *out, int64_t n_pos, int64_t packet_len, void *stream);
 /* keys[b][j] = key(seed, cw0 + b, j) >> 1 (int64, for the erasure selection). */
 int lch_gen_keys(lch_ctx *ctx, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
                  int64_t *keys, void *stream);

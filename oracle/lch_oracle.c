@@ -362,6 +362,70 @@ int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
     return rc;
 }
 
+/* General k: the reference's decode algorithm (rs.py:125-148)
+ * without the power-of-two restriction of rs.py:43-44, evaluated at every
+ * erased position.  full[n] = received with each erased j replaced by
+ * Phi^d(j) / Pi'(j).  Phi = f * Pi has degree < k + |E| <= n, so the n-point
+ * transforms recover f at the erasures for any k. */
+int orc_recover_all(const orc_ctx *c, const uint16_t *received, const uint8_t *erased,
+                    uint16_t *full) {
+    uint32_t n = c->order;
+    if (c->max_h < n) return ORC_EINVAL;
+    uint32_t cnt = 0;
+    for (uint32_t j = 0; j < n; ++j) cnt += erased[j] ? 1 : 0;
+    memcpy(full, received, sizeof(uint16_t) * n);
+    if (cnt == 0) return ORC_OK;
+    if (cnt == n) return ORC_EINVAL; /* walsh.py:92-93: at least one survivor */
+    uint32_t *mixed = (uint32_t *)malloc(sizeof(uint32_t) * n);
+    uint16_t *phi = (uint16_t *)malloc(sizeof(uint16_t) * n);
+    uint16_t *dc = (uint16_t *)malloc(sizeof(uint16_t) * n);
+    if (!mixed || !phi || !dc) { free(mixed); free(phi); free(dc); return ORC_ENOMEM; }
+    int rc = orc_locator_logs(c, erased, mixed);
+    if (!rc) {
+        for (uint32_t j = 0; j < n; ++j)
+            phi[j] = erased[j] ? 0 : (uint16_t)orc_mul(c, received[j], c->exp[mixed[j]]);
+        rc = orc_inverse(c, phi, n, 0);
+        if (!rc) rc = orc_derivative(c, phi, dc, n);
+        if (!rc) rc = orc_forward(c, dc, n, 0);
+        if (!rc)
+            for (uint32_t j = 0; j < n; ++j)
+                if (erased[j]) full[j] = (uint16_t)orc_mul(c, dc[j], f_inv(c, c->exp[mixed[j]]));
+    }
+    free(mixed); free(phi); free(dc);
+    return rc;
+}
+
+/* Systematic encode for any 1 <= k <= n: erasure-decode E = [k, n) from the
+ * message (fact iii: equals orc_encode for power-of-two k). */
+int orc_encode_any(const orc_ctx *c, uint32_t k, const uint16_t *msg, uint16_t *codeword) {
+    uint32_t n = c->order;
+    if (k < 1 || k > n) return ORC_EINVAL;
+    uint16_t *rx = (uint16_t *)calloc(n, sizeof(uint16_t));
+    uint8_t *e = (uint8_t *)calloc(n, 1);
+    if (!rx || !e) { free(rx); free(e); return ORC_ENOMEM; }
+    memcpy(rx, msg, sizeof(uint16_t) * k);
+    for (uint32_t j = k; j < n; ++j) e[j] = 1;
+    int rc = orc_recover_all(c, rx, e, codeword);
+    free(rx); free(e);
+    return rc;
+}
+
+/* Decode for any 1 <= k <= n: out[k] = positions [0, k) of the recovered word. */
+int orc_decode_any(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                   const uint8_t *erased, uint16_t *out) {
+    uint32_t n = c->order;
+    if (k < 1 || k > n) return ORC_EINVAL;
+    uint32_t cnt = 0;
+    for (uint32_t j = 0; j < n; ++j) cnt += erased[j] ? 1 : 0;
+    if (cnt > n - k) return ORC_ETOOMANY;
+    uint16_t *full = (uint16_t *)malloc(sizeof(uint16_t) * n);
+    if (!full) return ORC_ENOMEM;
+    int rc = orc_recover_all(c, received, erased, full);
+    if (!rc) memcpy(out, full, sizeof(uint16_t) * k);
+    free(full);
+    return rc;
+}
+
 /* ------------------------------------------------------------------------ */
 /* batched drivers (thread pool over codewords)                              */
 
@@ -384,14 +448,18 @@ static void *run_job(void *arg) {
     uint32_t n = c->order;
     j->rc = ORC_OK;
     uint16_t *cw = NULL;
-    if (j->op == 0) cw = (uint16_t *)malloc(sizeof(uint16_t) * n);
+    if (j->op == 0 || j->op == 3) cw = (uint16_t *)malloc(sizeof(uint16_t) * n);
     for (int64_t b = j->begin; b < j->end && j->rc == ORC_OK; ++b) {
         if (j->op == 0) {
             j->rc = orc_encode(c, j->k, j->in + b * j->k, cw);
             memcpy(j->out + b * (int64_t)(n - j->k), cw + j->k, sizeof(uint16_t) * (n - j->k));
-        } else if (j->op == 1) {
+        } else if (j->op == 3) {
+            j->rc = orc_encode_any(c, j->k, j->in + b * j->k, cw);
+            memcpy(j->out + b * (int64_t)(n - j->k), cw + j->k, sizeof(uint16_t) * (n - j->k));
+        } else if (j->op == 1 || j->op == 4) {
             const uint8_t *e = j->erased + (j->shared ? 0 : b * (int64_t)n);
-            j->rc = orc_decode(c, j->k, j->in + b * (int64_t)n, e, j->out + b * j->k);
+            j->rc = (j->op == 1 ? orc_decode : orc_decode_any)(c, j->k, j->in + b * (int64_t)n, e,
+                                                               j->out + b * j->k);
         } else {
             uint16_t *a = j->inout + b * (int64_t)j->h;
             j->rc = j->inverse ? orc_inverse(c, a, j->h, j->shift) : orc_forward(c, a, j->h, j->shift);
@@ -436,6 +504,24 @@ int orc_decode_batch(const orc_ctx *c, uint32_t k, const uint16_t *received,
     job_t p;
     memset(&p, 0, sizeof(p));
     p.c = c; p.op = 1; p.k = k; p.in = received; p.out = out;
+    p.erased = erased; p.shared = shared_pattern;
+    return run_pool(p, batch, nthreads);
+}
+
+int orc_encode_any_batch(const orc_ctx *c, uint32_t k, const uint16_t *msg,
+                         uint16_t *parity, int64_t batch, int nthreads) {
+    job_t p;
+    memset(&p, 0, sizeof(p));
+    p.c = c; p.op = 3; p.k = k; p.in = msg; p.out = parity;
+    return run_pool(p, batch, nthreads);
+}
+
+int orc_decode_any_batch(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                         const uint8_t *erased, int shared_pattern, uint16_t *out,
+                         int64_t batch, int nthreads) {
+    job_t p;
+    memset(&p, 0, sizeof(p));
+    p.c = c; p.op = 4; p.k = k; p.in = received; p.out = out;
     p.erased = erased; p.shared = shared_pattern;
     return run_pool(p, batch, nthreads);
 }

@@ -61,12 +61,26 @@ int orc_encode(const orc_ctx *c, uint32_t k, const uint16_t *msg, uint16_t *code
 int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
                const uint8_t *erased, uint16_t *out);
 
+/* General k, composed from the reference primitives:
+ * recover every erased position (rs.py:125-148 evaluated on all of E),
+ * systematic encode = erasure-decode of E = [k, n), decode = positions [0, k). */
+int orc_recover_all(const orc_ctx *c, const uint16_t *received, const uint8_t *erased,
+                    uint16_t *full);
+int orc_encode_any(const orc_ctx *c, uint32_t k, const uint16_t *msg, uint16_t *codeword);
+int orc_decode_any(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                   const uint8_t *erased, uint16_t *out);
+
 /* Batched drivers with a thread pool over codewords (CPU baseline). */
 int orc_encode_batch(const orc_ctx *c, uint32_t k, const uint16_t *msg,
                      uint16_t *parity, int64_t batch, int nthreads);
 int orc_decode_batch(const orc_ctx *c, uint32_t k, const uint16_t *received,
                      const uint8_t *erased, int shared_pattern, uint16_t *out,
                      int64_t batch, int nthreads);
+int orc_encode_any_batch(const orc_ctx *c, uint32_t k, const uint16_t *msg,
+                         uint16_t *parity, int64_t batch, int nthreads);
+int orc_decode_any_batch(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                         const uint8_t *erased, int shared_pattern, uint16_t *out,
+                         int64_t batch, int nthreads);
 int orc_transform_batch(const orc_ctx *c, uint16_t *a, uint32_t h, uint32_t shift,
                         int inverse, int64_t batch, int nthreads);
 

@@ -55,6 +55,11 @@ def lib() -> ctypes.CDLL:
         L.orc_encode_batch.argtypes = [P, u32, U16P, U16P, i64, i32]
         L.orc_decode_batch.argtypes = [P, u32, U16P, U8P, i32, U16P, i64, i32]
         L.orc_transform_batch.argtypes = [P, U16P, u32, u32, i32, i64, i32]
+        L.orc_recover_all.argtypes = [P, U16P, U8P, U16P]
+        L.orc_encode_any.argtypes = [P, u32, U16P, U16P]
+        L.orc_decode_any.argtypes = [P, u32, U16P, U8P, U16P]
+        L.orc_encode_any_batch.argtypes = [P, u32, U16P, U16P, i64, i32]
+        L.orc_decode_any_batch.argtypes = [P, u32, U16P, U8P, i32, U16P, i64, i32]
         L.orc_mix64.argtypes = [u64]
         L.orc_mix64.restype = u64
         L.orc_key.argtypes = [u64, u64, u64]
@@ -175,6 +180,45 @@ class Oracle:
         out = np.zeros((rx.shape[0], k), np.uint16)
         _check(lib().orc_decode_batch(self._h, k, _p(rx), _p(e), shared, _p(out),
                                       rx.shape[0], nthreads))
+        return out
+
+
+    # -- general k: composition of the reference's primitives --
+
+    def recover_all(self, received, erased_mask) -> np.ndarray:
+        rx = np.ascontiguousarray(received, dtype=np.uint16)
+        e = np.ascontiguousarray(erased_mask, dtype=np.uint8)
+        out = np.zeros(self.n, np.uint16)
+        _check(lib().orc_recover_all(self._h, _p(rx), _p(e), _p(out)))
+        return out
+
+    def encode_any(self, k: int, msg) -> np.ndarray:
+        m = np.ascontiguousarray(msg, dtype=np.uint16)
+        cw = np.zeros(self.n, np.uint16)
+        _check(lib().orc_encode_any(self._h, k, _p(m), _p(cw)))
+        return cw
+
+    def decode_any(self, k: int, received, erased_mask) -> np.ndarray:
+        rx = np.ascontiguousarray(received, dtype=np.uint16)
+        e = np.ascontiguousarray(erased_mask, dtype=np.uint8)
+        out = np.zeros(k, np.uint16)
+        _check(lib().orc_decode_any(self._h, k, _p(rx), _p(e), _p(out)))
+        return out
+
+    def encode_any_batch(self, k: int, msgs: np.ndarray, nthreads: int = 1) -> np.ndarray:
+        m = np.ascontiguousarray(msgs, dtype=np.uint16)
+        par = np.zeros((m.shape[0], self.n - k), np.uint16)
+        _check(lib().orc_encode_any_batch(self._h, k, _p(m), _p(par), m.shape[0], nthreads))
+        return par
+
+    def decode_any_batch(self, k: int, received: np.ndarray, erased: np.ndarray,
+                         nthreads: int = 1) -> np.ndarray:
+        rx = np.ascontiguousarray(received, dtype=np.uint16)
+        e = np.ascontiguousarray(erased, dtype=np.uint8)
+        shared = int(e.ndim == 1)
+        out = np.zeros((rx.shape[0], k), np.uint16)
+        _check(lib().orc_decode_any_batch(self._h, k, _p(rx), _p(e), shared, _p(out),
+                                          rx.shape[0], nthreads))
         return out
 
 

@@ -52,7 +52,11 @@ def _load() -> ctypes.CDLL:
         "lch_locator": ([P, P, i64, P, P, P], i32),
         "lch_encode": ([P, P, i64, P, i64, i64, i32, i64, P], i32),
         "lch_decode": ([P, P, i64, P, i32, P, i64, i64, i32, i64, P, P], i32),
+        "lch_encode_k": ([P, P, i64, P, i64, i64, i64, i64, P], i32),
+        "lch_decode_k": ([P, P, i64, P, i32, P, i64, i64, i64, i64, P, P], i32),
+        "lch_set_scratch_limit": ([P, u64], i32),
         "lch_gen_symbols": ([P, u64, u64, i64, i64, P, i64, P], i32),
+        "lch_gen_packets": ([P, u64, u64, i64, i64, P, i64, i64, P], i32),
         "lch_gen_keys": ([P, u64, u64, i64, i64, P, P], i32),
         "lch_launch_count": ([P], i64),
     }

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/lch.h"
@@ -24,6 +25,8 @@ struct lch_ctx {
   uint16_t *d_b_lo = nullptr;  // b_prod[j mod 2^(r-1)] for j < 2^r (decode derivative)
   uint32_t *d_fwht_log = nullptr;
   int64_t launches = 0;
+  size_t scratch_limit = size_t(4) << 30;
+  std::vector<std::pair<int64_t, uint16_t *>> enc_tabs;  // encode-by-decode tables per k
   std::mutex mu;
 };
 
@@ -463,6 +466,7 @@ void lch_destroy(lch_ctx *c) {
     cudaFree(c->d_log);
     cudaFree(c->d_fwht_log);
     cudaFree(c->d_b_lo);
+    for (auto &e : c->enc_tabs) cudaFree(e.second);
   }
   delete c;
 }
@@ -486,11 +490,152 @@ int lch_get_tables(const lch_ctx *c, uint16_t *log, uint16_t *exp, uint16_t *w_h
 
 int64_t lch_launch_count(const lch_ctx *c) { return c ? c->launches : 0; }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Layouts and lane chunking.
+//
+// Row layout (packet_len == 0): lane b = row b, symbol j at ptr[b * stride + j].
+// Packet layout (packet_len = P > 0, P % 1024 == 0): lane b = (stripe group
+// b / P, packet offset b % P), symbol j at ptr[((b / P) * stride + j) * P + b % P];
+// the stride counts positions per stripe group.  Each 1024-lane bit-sliced
+// group then lies inside one stripe group, so per-group tables are uniform.
+
+static int check_layout(const void *p, int64_t batch, int64_t pkt) {
+  if (pkt < 0) return LCH_EINVAL;
+  if (pkt == 0) return LCH_OK;
+  if (pkt % GROUP || batch % pkt) return LCH_EINVAL;
+  if (p && reinterpret_cast<uintptr_t>(p) % 16) return LCH_EINVAL;
+  return LCH_OK;
+}
+
+static RawIO make_io(const uint16_t *ptr, int64_t stride, int64_t pkt) {
+  uint16_t *q = const_cast<uint16_t *>(ptr);
+  return pkt ? make_raw(q, 0, pkt, stride) : make_raw(q, stride);
+}
+
+// pointer to position j of lane 0
+static uint16_t *at_pos(const uint16_t *ptr, int64_t j, int64_t pkt) {
+  return const_cast<uint16_t *>(ptr) + (pkt ? j * pkt : j);
+}
+
+// the same I/O descriptor for the lanes starting at b0
+static RawIO shift_io(RawIO io, int64_t b0) {
+  if (io.pkt) {
+    const int64_t g0 = b0 / io.pkt;
+    io.ptr += g0 * io.npos * io.pkt;
+    if (io.merge_src) io.merge_src += g0 * io.merge_stride * io.pkt;
+    if (io.merge_bits) io.merge_bits += g0 * io.bits_stride;
+  } else {
+    io.ptr += b0 * io.row_stride;
+    if (io.merge_src) io.merge_src += b0 * io.merge_stride;
+    if (io.merge_bits) io.merge_bits += b0 * io.bits_stride;
+    if (io.pinv_log) io.pinv_log += b0 * io.pinv_stride;
+  }
+  return io;
+}
+
+static size_t bs_lane_bytes(int R, int lgH) { return (size_t(1) << lgH) * size_t(R) / 8; }
+
+// lanes per chunk so that `lane_bytes` of scratch per lane fit the budget
+static int64_t chunk_lanes(const lch_ctx *c, int64_t batch, int64_t pkt, size_t lane_bytes) {
+  const int64_t unit = pkt ? pkt : GROUP;
+  int64_t ch = lane_bytes ? int64_t(c->scratch_limit / lane_bytes) : batch;
+  ch = std::max<int64_t>(unit, ch / unit * unit);
+  return std::min(ch, batch);
+}
+
+static int ceil_lg(int64_t k) {
+  int l = 0;
+  while ((int64_t(1) << l) < k) ++l;
+  return l;
+}
+
+// Erasure pipeline with per-position tables shared by a batch (or by each
+// stripe group: row stride *_stride per group), rs.py:130-148:
+//   Phi = rx * pi_row -> n-point inverse -> derivative -> 2^lg_out-point
+//   forward -> * pinv, written to out_io's window (merging survivors when
+//   out_io.merge_src is set).  For lg_out <= r - 1 the XOR-only top inverse
+//   level is folded into the derivative gather (T_j = W'_(r-1)(y_j + y_(j+n/2))
+//   + sum_(l<r-1, bit l of j clear) y_(j|2^l), y_j = B_(j mod n/2) x_j); for
+//   lg_out = r (k > n/2, or encode-by-decode) the plain schedule runs.
+template <int R, uint32_t POLY>
+static int erasure_core(lch_ctx *c, const RawIO &in0, const RawIO &out0, const uint16_t *pi_row,
+                        int64_t pi_stride, const uint16_t *pinv, int64_t pinv_stride, int lg_out,
+                        int64_t batch, int64_t pkt, cudaStream_t s) {
+  const int r = c->t.r;
+  const bool folded = lg_out <= r - 1;
+  const int64_t ch = chunk_lanes(c, batch, pkt, bs_lane_bytes(R, r) + 2 * bs_lane_bytes(R, lg_out));
+  Scratch sc(s);
+  uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
+  LCH_TRY(sc.alloc(x, bs_bytes(R, ch, r) / 16));
+  LCH_TRY(sc.alloc(t, bs_bytes(R, ch, lg_out) / 16));
+  LCH_TRY(sc.alloc(t1, bs_bytes(R, ch, lg_out) / 16));
+  for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+    const int64_t nb = std::min(ch, batch - b0);
+    const int64_t g0 = pkt ? b0 / pkt : 0;
+    RawIO in_io = shift_io(in0, b0), out_io = shift_io(out0, b0);
+    std::vector<LOp> a = {{OP_SCALE, 0, 0, pi_row + g0 * pi_stride, pi_stride}};
+    const int ninv = folded ? r - 1 : r;
+    for (int i = 0; i < ninv; ++i) a.push_back({OP_INV, i, 0u, nullptr});
+    a.push_back({OP_SCALE, 0, 0, folded ? c->d_b_lo : c->d_b_prod});
+    auto plan_a = plan_passes(a, r, true, false);
+    // the last inverse pass also sums the gather over its own tile bits
+    LCH_TRY((run_plan<R, POLY>(c, plan_a, r, nb, &in_io, nullptr, nullptr, x, s, t1, lg_out, pkt)));
+    std::vector<int> rest;
+    const auto &lb = plan_a.back().bits;
+    for (int b = 0; b < ninv; ++b)
+      if (std::find(lb.begin(), lb.end(), b) == lb.end()) rest.push_back(b);
+    if (folded) rest.push_back(r - 1);
+    LCH_TRY((run_gather<R, POLY>(c, x, t, r, lg_out, nb, rest, folded ? r - 1 : -1,
+                                 folded ? c->t.w_prime[r - 1] : 0u, t1, s)));
+    std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
+    for (int i = lg_out - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
+    b.push_back({OP_SCALE, 0, 0, pinv + g0 * pinv_stride, pinv_stride});
+    LCH_TRY((run_plan<R, POLY>(c, plan_passes(b, lg_out, false, true), lg_out, nb, nullptr, t, &out_io,
+                               t, s, nullptr, 0, pkt)));
+  }
+  return LCH_OK;
+}
+
+// per-pattern erasure counts (host), from host_counts or a device reduction
+static int pattern_counts(lch_ctx *c, const uint32_t *bits, int64_t np, int words,
+                          const int64_t *host_counts, std::vector<int64_t> &counts,
+                          cudaStream_t s) {
+  counts.assign(size_t(np), 0);
+  if (host_counts) {
+    std::memcpy(counts.data(), host_counts, sizeof(int64_t) * size_t(np));
+    return LCH_OK;
+  }
+  Scratch sc(s);
+  int64_t *dc = nullptr;
+  LCH_TRY(sc.alloc(dc, size_t(np)));
+  LCH_TRY(cu(launch_count_bits(bits, np, words, dc, s)));
+  c->launches++;
+  LCH_TRY(cu(cudaMemcpyAsync(counts.data(), dc, sizeof(int64_t) * size_t(np), cudaMemcpyDeviceToHost, s)));
+  return cu(cudaStreamSynchronize(s));
+}
+
+// locator logs -> pi_row [np][n] and pinv [np][kf] (rs.py:125-148)
+static int erasure_tables(lch_ctx *c, const uint32_t *bits, int64_t np, int64_t kf, Scratch &sc,
+                          uint16_t *&pi_row, uint16_t *&pinv, cudaStream_t s) {
+  const int64_t n = int64_t(c->t.order);
+  uint16_t *logs = nullptr;
+  LCH_TRY(sc.alloc(logs, size_t(np * n)));
+  LCH_TRY(sc.alloc(pi_row, size_t(np * n)));
+  LCH_TRY(sc.alloc(pinv, size_t(np * kf)));
+  LCH_TRY(locator_impl(c, bits, np, nullptr, logs, s));
+  LCH_TRY(cu(launch_decode_rows(logs, bits, c->d_exp, c->t.m, uint32_t(n), uint32_t(kf), pi_row, pinv,
+                                np, s)));
+  c->launches++;
+  return LCH_OK;
+}
+
 static int transform_impl(lch_ctx *c, uint16_t *data, int64_t batch, int64_t stride, int lg_h,
-                          uint32_t shift, int64_t packet_len, void *stream, bool inverse) {
+                          uint32_t shift, int64_t pkt, void *stream, bool inverse) {
   if (!c || lg_h < 0 || lg_h > c->max_lg_h || batch < 0) return LCH_EINVAL;
   if (shift >= c->t.order) return LCH_EINVAL;
-  if (packet_len != 0) return LCH_EUNSUPPORTED;
+  LCH_TRY(check_layout(data, batch, pkt));
   const int64_t h = int64_t(1) << lg_h;
   if (stride < h) return LCH_EINVAL;
   LCH_TRY(ensure_device(c));
@@ -505,13 +650,270 @@ static int transform_impl(lch_ctx *c, uint16_t *data, int64_t batch, int64_t str
     constexpr int R = decltype(RC)::value;
     constexpr uint32_t P = decltype(PC)::value;
     auto plan = plan_passes(ops, lg_h, true, true);
-    RawIO io = make_raw(data, stride);
+    const int64_t ch = plan.size() > 1 ? chunk_lanes(c, batch, pkt, bs_lane_bytes(R, lg_h)) : batch;
     Scratch sc(s);
     uint4 *work = nullptr;
-    if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, batch, lg_h) / 16));
-    return run_plan<R, P>(c, plan, lg_h, batch, &io, nullptr, &io, work, s);
+    if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, ch, lg_h) / 16));
+    const RawIO io0 = make_io(data, stride, pkt);
+    for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+      RawIO io = shift_io(io0, b0);
+      LCH_TRY((run_plan<R, P>(c, plan, lg_h, std::min(ch, batch - b0), &io, nullptr, &io, work, s,
+                              nullptr, 0, pkt)));
+    }
+    return LCH_OK;
   });
 }
+
+// Systematic encode for power-of-two k (rs.py:85-96).
+static int encode_pow2(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
+                       int64_t stride_out, int64_t batch, int lg_k, int64_t pkt, cudaStream_t s) {
+  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k, nb = n / k;
+  if (nb == 1) return LCH_OK;
+  if (lg_k == 0) {
+    // 1-point transforms are the identity: every parity symbol is the message
+    const int64_t rows = pkt ? batch / pkt : batch, w = pkt ? pkt : 1;
+    const size_t sp_out = size_t(pkt ? stride_out * pkt : stride_out) * 2;
+    const size_t sp_in = size_t(pkt ? stride_in * pkt : stride_in) * 2;
+    for (int64_t i = 1; i < nb; ++i)
+      LCH_TRY(cu(cudaMemcpy2DAsync(at_pos(parity, i - 1, pkt), sp_out, msg, sp_in, size_t(w) * 2,
+                                   size_t(rows), cudaMemcpyDeviceToDevice, s)));
+    return LCH_OK;
+  }
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    Scratch sc(s);
+    const RawIO in0 = make_io(msg, stride_in, pkt);
+    // rs.py:91 coefficients by a k-point inverse at shift 0
+    std::vector<LOp> inv;
+    for (int i = 0; i < lg_k; ++i) inv.push_back({OP_INV, i, 0u, nullptr});
+    if (nb == 2) {
+      // rs.py:93-95 with one parity block: fuse inverse and forward(shift k)
+      std::vector<LOp> ops = inv;
+      for (int i = lg_k - 1; i >= 0; --i) ops.push_back({OP_FWD, i, hs_of(c, i, uint32_t(k)), nullptr});
+      auto plan = plan_passes(ops, lg_k, true, true);
+      const int64_t ch = plan.size() > 1 ? chunk_lanes(c, batch, pkt, bs_lane_bytes(R, lg_k)) : batch;
+      uint4 *work = nullptr;
+      if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, ch, lg_k) / 16));
+      const RawIO out0 = make_io(parity, stride_out, pkt);
+      for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+        RawIO in_io = shift_io(in0, b0), out_io = shift_io(out0, b0);
+        LCH_TRY((run_plan<R, P>(c, plan, lg_k, std::min(ch, batch - b0), &in_io, nullptr, &out_io, work,
+                                s, nullptr, 0, pkt)));
+      }
+      return LCH_OK;
+    }
+    const int64_t ch = chunk_lanes(c, batch, pkt, 2 * bs_lane_bytes(R, lg_k));
+    uint4 *coef = nullptr, *work = nullptr;
+    LCH_TRY(sc.alloc(coef, bs_bytes(R, ch, lg_k) / 16));
+    LCH_TRY(sc.alloc(work, bs_bytes(R, ch, lg_k) / 16));
+    for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+      const int64_t bn = std::min(ch, batch - b0);
+      RawIO in_io = shift_io(in0, b0);
+      LCH_TRY((run_plan<R, P>(c, plan_passes(inv, lg_k, true, false), lg_k, bn, &in_io, nullptr,
+                              nullptr, coef, s, nullptr, 0, pkt)));
+      for (int64_t blk = 1; blk < nb; ++blk) {
+        std::vector<LOp> fwd;
+        const uint32_t shift = uint32_t(blk * k);
+        for (int i = lg_k - 1; i >= 0; --i) fwd.push_back({OP_FWD, i, hs_of(c, i, shift), nullptr});
+        RawIO out_io = shift_io(make_io(at_pos(parity, (blk - 1) * k, pkt), stride_out, pkt), b0);
+        LCH_TRY((run_plan<R, P>(c, plan_passes(fwd, lg_k, false, true), lg_k, bn, nullptr, coef,
+                                &out_io, work, s, nullptr, 0, pkt)));
+      }
+    }
+    return LCH_OK;
+  });
+}
+
+// Encode-by-erasure-decode tables for E = [k, n): pi_row [n], pinv [n]
+// (cached per k on the context).
+static int encode_tables(lch_ctx *c, int64_t k, const uint16_t *&pi_row, const uint16_t *&pinv,
+                         cudaStream_t s) {
+  const int64_t n = int64_t(c->t.order);
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    for (auto &e : c->enc_tabs)
+      if (e.first == k) {
+        pi_row = e.second;
+        pinv = e.second + n;
+        return LCH_OK;
+      }
+  }
+  const int words = int(std::max<int64_t>(n / 32, 1));
+  std::vector<uint32_t> hb(size_t(words), 0u);
+  for (int64_t j = k; j < n; ++j) hb[size_t(j >> 5)] |= 1u << (j & 31);
+  uint16_t *tab = nullptr;
+  LCH_TRY(cu(cudaMalloc(&tab, size_t(2 * n) * 2)));
+  int rc;
+  {
+    Scratch sc(s);
+    uint32_t *db = nullptr;
+    uint16_t *pr = nullptr, *pv = nullptr;
+    rc = sc.alloc(db, size_t(words));
+    if (rc == LCH_OK) rc = cu(cudaMemcpyAsync(db, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice, s));
+    if (rc == LCH_OK) rc = erasure_tables(c, db, 1, n, sc, pr, pv, s);
+    if (rc == LCH_OK) rc = cu(cudaMemcpyAsync(tab, pr, size_t(n) * 2, cudaMemcpyDeviceToDevice, s));
+    if (rc == LCH_OK) rc = cu(cudaMemcpyAsync(tab + n, pv, size_t(n) * 2, cudaMemcpyDeviceToDevice, s));
+  }
+  if (rc == LCH_OK) rc = cu(cudaStreamSynchronize(s));
+  if (rc != LCH_OK) {
+    cudaFree(tab);
+    return rc;
+  }
+  std::lock_guard<std::mutex> g(c->mu);
+  c->enc_tabs.push_back({k, tab});
+  pi_row = tab;
+  pinv = tab + n;
+  return LCH_OK;
+}
+
+static int encode_any(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
+                      int64_t stride_out, int64_t batch, int64_t k, int64_t pkt, void *stream) {
+  if (!c || batch < 0) return LCH_EINVAL;
+  const int64_t n = int64_t(c->t.order);
+  if (k < 1 || k > n) return LCH_EINVAL;
+  LCH_TRY(check_layout(msg, batch, pkt));
+  LCH_TRY(check_layout(parity, batch, pkt));
+  if (stride_in < k || (k < n && stride_out < n - k)) return LCH_EINVAL;
+  const bool pow2 = (k & (k - 1)) == 0;
+  if (pow2 && ceil_lg(k) > c->max_lg_h) return LCH_EINVAL;  // rs.py:162-163
+  if (!pow2 && c->max_lg_h < c->t.r) return LCH_EINVAL;      // n-point transforms
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || k == n) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pow2) return encode_pow2(c, msg, stride_in, parity, stride_out, batch, ceil_lg(k), pkt, s);
+  const uint16_t *pi_row = nullptr, *pinv = nullptr;
+  LCH_TRY(encode_tables(c, k, pi_row, pinv, s));
+  RawIO in_io = make_io(msg, stride_in, pkt);
+  in_io.pos_hi = k;  // positions >= k (erased) read as zero
+  RawIO out_io = make_io(parity, stride_out, pkt);
+  out_io.pos_lo = k;  // parity = positions [k, n)
+  out_io.pos_hi = n;
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    return erasure_core<R, P>(c, in_io, out_io, pi_row, 0, pinv, 0, c->t.r, batch, pkt, s);
+  });
+}
+
+// Decode with one erasure pattern per row (rs.decode row by row): batched
+// locator whose epilogue writes phi = rx * Pi_bar (rs.py:130-134) and
+// -log Pi' (rs.py:141-148); the shared transform pipeline without the
+// per-position scaling; the output epilogue divides erased symbols by Pi'.
+static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in,
+                               const uint32_t *bits, uint16_t *out, int64_t stride_out,
+                               int64_t batch, int64_t k, cudaStream_t s) {
+  const int r = c->t.r;
+  const int64_t n = int64_t(c->t.order);
+  const int lgo = std::max(ceil_lg(k), 1);
+  const int64_t kf = int64_t(1) << lgo;  // forward length (first kf outputs)
+  if (lgo > r - 1) return LCH_EUNSUPPORTED;
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    Scratch sc(s);
+    uint16_t *phi = nullptr, *pinv_log = nullptr;
+    LCH_TRY(sc.alloc(phi, size_t(batch) * size_t(stride_in)));
+    LCH_TRY(sc.alloc(pinv_log, size_t(batch) * size_t(kf)));
+    DecodeEpi epi;
+    epi.rx = rx;
+    epi.rx_stride = stride_in;  // phi is written with the received words' row stride
+    epi.phi = phi;
+    epi.pinv_log = pinv_log;
+    epi.k = uint32_t(kf);  // bound and row stride of pinv_log
+    LCH_TRY(locator_impl(c, bits, batch, nullptr, nullptr, s, &epi));
+    const int64_t ch = chunk_lanes(c, batch, 0, bs_lane_bytes(R, r) + 2 * bs_lane_bytes(R, lgo));
+    uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
+    LCH_TRY(sc.alloc(x, bs_bytes(R, ch, r) / 16));
+    LCH_TRY(sc.alloc(t, bs_bytes(R, ch, lgo) / 16));
+    LCH_TRY(sc.alloc(t1, bs_bytes(R, ch, lgo) / 16));
+    const RawIO in0 = make_raw(phi, stride_in);
+    RawIO out0 = make_raw(out, stride_out);
+    out0.pos_hi = k;
+    out0.merge_src = rx;
+    out0.merge_stride = stride_in;
+    out0.merge_bits = bits;
+    out0.bits_stride = n / 32;
+    out0.pinv_log = pinv_log;
+    out0.pinv_stride = kf;
+    out0.log_tab = c->d_log;
+    out0.exp_tab = c->d_exp;
+    out0.mord = c->t.m;
+    out0.vec = out0.vec && (reinterpret_cast<uintptr_t>(rx) % 16 == 0) && (stride_in % 8 == 0);
+    for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+      const int64_t nb = std::min(ch, batch - b0);
+      RawIO in_io = shift_io(in0, b0), out_io = shift_io(out0, b0);
+      std::vector<LOp> a;
+      for (int i = 0; i + 1 < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
+      a.push_back({OP_SCALE, 0, 0, c->d_b_lo});
+      auto plan_a = plan_passes(a, r, true, false);
+      LCH_TRY((run_plan<R, P>(c, plan_a, r, nb, &in_io, nullptr, nullptr, x, s, t1, lgo)));
+      std::vector<int> rest;
+      const auto &lb = plan_a.back().bits;
+      for (int b = 0; b + 1 < r; ++b)
+        if (std::find(lb.begin(), lb.end(), b) == lb.end()) rest.push_back(b);
+      rest.push_back(r - 1);
+      LCH_TRY((run_gather<R, P>(c, x, t, r, lgo, nb, rest, r - 1, c->t.w_prime[r - 1], t1, s)));
+      std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
+      for (int i = lgo - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
+      LCH_TRY((run_plan<R, P>(c, plan_passes(b, lgo, false, true), lgo, nb, nullptr, t, &out_io, t, s)));
+    }
+    return LCH_OK;
+  });
+}
+
+static int decode_any(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t *bits,
+                      int shared, uint16_t *out, int64_t stride_out, int64_t batch, int64_t k,
+                      int64_t pkt, const int64_t *host_counts, void *stream) {
+  if (!c || batch < 0 || !bits) return LCH_EINVAL;
+  const int r = c->t.r;
+  const int64_t n = int64_t(c->t.order);
+  if (k < 1 || k > n) return LCH_EINVAL;
+  LCH_TRY(check_layout(rx, batch, pkt));
+  LCH_TRY(check_layout(out, batch, pkt));
+  if (stride_in < n || stride_out < k) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int words = int(std::max<int64_t>(n / 32, 1));
+  const int64_t np = shared ? 1 : (pkt ? batch / pkt : batch);
+  std::vector<int64_t> counts;
+  LCH_TRY(pattern_counts(c, bits, np, words, host_counts, counts, s));
+  int64_t maxc = 0;
+  for (int64_t v : counts) maxc = std::max(maxc, v);
+  if (maxc > n - k) return LCH_ETOOMANY;  // rs.py:121-123
+  if (maxc == 0) {                        // rs.py:119-120
+    const int64_t rows = pkt ? batch / pkt : batch, w = pkt ? k * pkt : k;
+    const size_t sp_out = size_t(pkt ? stride_out * pkt : stride_out) * 2;
+    const size_t sp_in = size_t(pkt ? stride_in * pkt : stride_in) * 2;
+    return cu(cudaMemcpy2DAsync(out, sp_out, rx, sp_in, size_t(w) * 2, size_t(rows),
+                                cudaMemcpyDeviceToDevice, s));
+  }
+  if (c->max_lg_h < r) return LCH_EINVAL;  // n-point transforms (transform.py:63-64)
+  if (!shared && !pkt) return decode_per_codeword(c, rx, stride_in, bits, out, stride_out, batch, k, s);
+  const int lgo = std::max(ceil_lg(k), 1);
+  const int64_t kf = int64_t(1) << lgo;
+  Scratch sc(s);
+  uint16_t *pi_row = nullptr, *pinv = nullptr;
+  // rs.py:125 locator values, one per pattern
+  LCH_TRY(erasure_tables(c, bits, np, kf, sc, pi_row, pinv, s));
+  const RawIO in_io = make_io(rx, stride_in, pkt);
+  RawIO out_io = make_io(out, stride_out, pkt);
+  out_io.pos_hi = k;
+  out_io.merge_src = rx;
+  out_io.merge_stride = stride_in;
+  out_io.merge_bits = bits;
+  out_io.bits_stride = shared ? 0 : words;
+  if (!pkt) out_io.vec = out_io.vec && (reinterpret_cast<uintptr_t>(rx) % 16 == 0) && (stride_in % 8 == 0);
+  return dispatch(c, [&](auto RC, auto PC) -> int {
+    constexpr int R = decltype(RC)::value;
+    constexpr uint32_t P = decltype(PC)::value;
+    return erasure_core<R, P>(c, in_io, out_io, pi_row, shared ? 0 : n, pinv, shared ? 0 : kf, lgo, batch,
+                              pkt, s);
+  });
+}
+
+extern "C" {
 
 int lch_forward(lch_ctx *c, uint16_t *data, int64_t batch, int64_t stride, int lg_h, uint32_t shift,
                 int64_t packet_len, void *stream) {
@@ -526,33 +928,42 @@ int lch_inverse(lch_ctx *c, uint16_t *data, int64_t batch, int64_t stride, int l
 int lch_derivative(lch_ctx *c, const uint16_t *in, uint16_t *out, int64_t batch, int64_t stride,
                    int lg_h, int64_t packet_len, void *stream) {
   if (!c || lg_h < 0 || lg_h > c->max_lg_h || batch < 0) return LCH_EINVAL;
-  if (packet_len != 0) return LCH_EUNSUPPORTED;
-  const int64_t h = int64_t(1) << lg_h;
+  LCH_TRY(check_layout(in, batch, packet_len));
+  LCH_TRY(check_layout(out, batch, packet_len));
+  const int64_t h = int64_t(1) << lg_h, pkt = packet_len;
   if (stride < h) return LCH_EINVAL;
   LCH_TRY(ensure_device(c));
   if (batch == 0) return LCH_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (lg_h == 0)
-    return cu(cudaMemset2DAsync(out, size_t(stride) * 2, 0, 2, size_t(batch), s));
+  if (lg_h == 0) {
+    const int64_t rows = pkt ? batch / pkt : batch, w = pkt ? pkt : 1;
+    return cu(cudaMemset2DAsync(out, size_t(pkt ? stride * pkt : stride) * 2, 0, size_t(w) * 2,
+                                size_t(rows), s));
+  }
   return dispatch(c, [&](auto RC, auto PC) -> int {
     constexpr int R = decltype(RC)::value;
     constexpr uint32_t P = decltype(PC)::value;
+    const int64_t ch = chunk_lanes(c, batch, pkt, 2 * bs_lane_bytes(R, lg_h));
     Scratch sc(s);
     uint4 *x = nullptr, *t = nullptr;
-    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, lg_h) / 16));
-    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, lg_h) / 16));
-    RawIO in_io = make_raw(const_cast<uint16_t *>(in), stride);
-    RawIO out_io = make_raw(out, stride);
-    // derivative.py:56 scale by B_i, :60-70 gather-XOR, :73-76 scale by B_j^-1
-    std::vector<LOp> pre = {{OP_SCALE, 0, 0, c->d_b_prod}};
-    LCH_TRY((run_plan<R, P>(c, plan_passes(pre, lg_h, true, false), lg_h, batch, &in_io, nullptr,
-                            nullptr, x, s)));
+    LCH_TRY(sc.alloc(x, bs_bytes(R, ch, lg_h) / 16));
+    LCH_TRY(sc.alloc(t, bs_bytes(R, ch, lg_h) / 16));
+    const RawIO in0 = make_io(in, stride, pkt), out0 = make_io(out, stride, pkt);
     std::vector<int> all;
     for (int b = 0; b < lg_h; ++b) all.push_back(b);
-    LCH_TRY((run_gather<R, P>(c, x, t, lg_h, lg_h, batch, all, -1, 0u, nullptr, s)));
-    std::vector<LOp> post = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
-    return run_plan<R, P>(c, plan_passes(post, lg_h, false, true), lg_h, batch, nullptr, t, &out_io,
-                          t, s);
+    for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+      const int64_t nb = std::min(ch, batch - b0);
+      RawIO in_io = shift_io(in0, b0), out_io = shift_io(out0, b0);
+      // derivative.py:56 scale by B_i, :60-70 gather-XOR, :73-76 scale by B_j^-1
+      std::vector<LOp> pre = {{OP_SCALE, 0, 0, c->d_b_prod}};
+      LCH_TRY((run_plan<R, P>(c, plan_passes(pre, lg_h, true, false), lg_h, nb, &in_io, nullptr,
+                              nullptr, x, s)));
+      LCH_TRY((run_gather<R, P>(c, x, t, lg_h, lg_h, nb, all, -1, 0u, nullptr, s)));
+      std::vector<LOp> post = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
+      LCH_TRY((run_plan<R, P>(c, plan_passes(post, lg_h, false, true), lg_h, nb, nullptr, t, &out_io,
+                              t, s)));
+    }
+    return LCH_OK;
   });
 }
 
@@ -588,251 +999,36 @@ int lch_locator(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out,
 
 int lch_encode(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
                int64_t stride_out, int64_t batch, int lg_k, int64_t packet_len, void *stream) {
-  if (!c || batch < 0 || lg_k < 0 || lg_k > c->t.r) return LCH_EINVAL;
-  if (lg_k > c->max_lg_h) return LCH_EINVAL;  // rs.py:162-163
-  if (packet_len != 0) return LCH_EUNSUPPORTED;
-  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k, nb = n / k;
-  if (stride_in < k || (nb > 1 && stride_out < n - k)) return LCH_EINVAL;
-  LCH_TRY(ensure_device(c));
-  if (batch == 0 || nb == 1) return LCH_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (lg_k == 0) {
-    // 1-point transforms are the identity: every parity symbol is the message
-    for (int64_t i = 1; i < nb; ++i)
-      LCH_TRY(cu(cudaMemcpy2DAsync(parity + (i - 1), size_t(stride_out) * 2, msg, size_t(stride_in) * 2,
-                                   2, size_t(batch), cudaMemcpyDeviceToDevice, s)));
-    return LCH_OK;
-  }
-  return dispatch(c, [&](auto RC, auto PC) -> int {
-    constexpr int R = decltype(RC)::value;
-    constexpr uint32_t P = decltype(PC)::value;
-    Scratch sc(s);
-    RawIO in_io = make_raw(const_cast<uint16_t *>(msg), stride_in);
-    // rs.py:91 coefficients by a k-point inverse at shift 0
-    std::vector<LOp> inv;
-    for (int i = 0; i < lg_k; ++i) inv.push_back({OP_INV, i, 0u, nullptr});
-    if (nb == 2) {
-      // rs.py:93-95 with one parity block: fuse inverse and forward(shift k)
-      std::vector<LOp> ops = inv;
-      for (int i = lg_k - 1; i >= 0; --i) ops.push_back({OP_FWD, i, hs_of(c, i, uint32_t(k)), nullptr});
-      auto plan = plan_passes(ops, lg_k, true, true);
-      uint4 *work = nullptr;
-      if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, batch, lg_k) / 16));
-      RawIO out_io = make_raw(parity, stride_out);
-      return run_plan<R, P>(c, plan, lg_k, batch, &in_io, nullptr, &out_io, work, s);
-    }
-    uint4 *coef = nullptr, *work = nullptr;
-    LCH_TRY(sc.alloc(coef, bs_bytes(R, batch, lg_k) / 16));
-    LCH_TRY(sc.alloc(work, bs_bytes(R, batch, lg_k) / 16));
-    LCH_TRY((run_plan<R, P>(c, plan_passes(inv, lg_k, true, false), lg_k, batch, &in_io, nullptr,
-                            nullptr, coef, s)));
-    for (int64_t blk = 1; blk < nb; ++blk) {
-      std::vector<LOp> fwd;
-      const uint32_t shift = uint32_t(blk * k);
-      for (int i = lg_k - 1; i >= 0; --i) fwd.push_back({OP_FWD, i, hs_of(c, i, shift), nullptr});
-      RawIO out_io = make_raw(parity + (blk - 1) * k, stride_out);
-      LCH_TRY((run_plan<R, P>(c, plan_passes(fwd, lg_k, false, true), lg_k, batch, nullptr, coef,
-                              &out_io, work, s)));
-    }
-    return LCH_OK;
-  });
+  if (!c || lg_k < 0 || lg_k > c->t.r) return LCH_EINVAL;
+  return encode_any(c, msg, stride_in, parity, stride_out, batch, int64_t(1) << lg_k, packet_len,
+                    stream);
 }
 
-// Decode with one erasure pattern per codeword (rs.decode row by row):
-// batched locator whose epilogue writes phi = rx * Pi_bar (rs.py:130-134) and
-// -log Pi' (rs.py:141-148); the shared transform pipeline without the
-// per-position scaling; the output epilogue divides erased symbols by Pi'.
-static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in,
-                               const uint32_t *bits, uint16_t *out, int64_t stride_out,
-                               int64_t batch, int lg_k, const int64_t *host_counts,
-                               cudaStream_t s) {
-  const int r = c->t.r;
-  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k;
-  const int words = int(n / 32);
-  {
-    std::vector<int64_t> counts(size_t(batch), 0);
-    if (host_counts) {
-      std::memcpy(counts.data(), host_counts, sizeof(int64_t) * size_t(batch));
-    } else {
-      Scratch sc(s);
-      int64_t *dc = nullptr;
-      LCH_TRY(sc.alloc(dc, size_t(batch)));
-      LCH_TRY(cu(launch_count_bits(bits, batch, words, dc, s)));
-      c->launches++;
-      LCH_TRY(cu(cudaMemcpyAsync(counts.data(), dc, sizeof(int64_t) * size_t(batch),
-                                 cudaMemcpyDeviceToHost, s)));
-      LCH_TRY(cu(cudaStreamSynchronize(s)));
-    }
-    for (int64_t cnt : counts)
-      if (cnt > n - k) return LCH_ETOOMANY;  // rs.py:121-123
-  }
-  if (c->max_lg_h < r) return LCH_EINVAL;
-  return dispatch(c, [&](auto RC, auto PC) -> int {
-    constexpr int R = decltype(RC)::value;
-    constexpr uint32_t P = decltype(PC)::value;
-    Scratch sc(s);
-    const int lgk_out = std::max(lg_k, 1);
-    uint16_t *phi = nullptr, *pinv_log = nullptr;
-    LCH_TRY(sc.alloc(phi, size_t(batch) * size_t(n)));
-    LCH_TRY(sc.alloc(pinv_log, size_t(batch) * size_t(std::max<int64_t>(k, 2))));
-    DecodeEpi epi;
-    epi.rx = rx;
-    epi.rx_stride = stride_in;
-    epi.phi = phi;
-    epi.pinv_log = pinv_log;
-    epi.k = uint32_t(std::max<int64_t>(k, 2));  // bound and row stride of pinv_log
-    // phi is written with the received words' row stride
-    if (stride_in != n) {
-      uint16_t *phi2 = nullptr;
-      LCH_TRY(sc.alloc(phi2, size_t(batch) * size_t(stride_in)));
-      epi.phi = phi2;
-    }
-    LCH_TRY(locator_impl(c, bits, batch, nullptr, nullptr, s, &epi));
-    uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
-    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, r) / 16));
-    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, lgk_out) / 16));
-    LCH_TRY(sc.alloc(t1, bs_bytes(R, batch, lgk_out) / 16));
-    RawIO in_io = make_raw(epi.phi, stride_in);
-    std::vector<LOp> a;
-    for (int i = 0; i + 1 < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
-    a.push_back({OP_SCALE, 0, 0, c->d_b_lo});
-    auto plan_a = plan_passes(a, r, true, false);
-    LCH_TRY((run_plan<R, P>(c, plan_a, r, batch, &in_io, nullptr, nullptr, x, s, t1, lgk_out)));
-    std::vector<int> rest;
-    for (int b = 0; b + 1 < r; ++b)
-      if (std::find(plan_a.back().bits.begin(), plan_a.back().bits.end(), b) == plan_a.back().bits.end())
-        rest.push_back(b);
-    rest.push_back(r - 1);
-    LCH_TRY((run_gather<R, P>(c, x, t, r, lgk_out, batch, rest, r - 1, c->t.w_prime[r - 1], t1, s)));
-    std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
-    for (int i = lg_k - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
-    const int lgo = std::max(lg_k, 1);
-    uint16_t *dst = out;
-    int64_t dst_stride = stride_out;
-    uint16_t *tmp = nullptr;
-    if (lg_k == 0) {  // 2-column scratch output, column 0 copied below
-      LCH_TRY(sc.alloc(tmp, size_t(batch) * 8));
-      dst = tmp;
-      dst_stride = 8;
-    }
-    RawIO out_io = make_raw(dst, dst_stride);
-    out_io.merge_src = rx;
-    out_io.merge_stride = stride_in;
-    out_io.merge_bits = bits;
-    out_io.bits_stride = words;
-    out_io.pinv_log = pinv_log;
-    out_io.pinv_stride = std::max<int64_t>(k, 2);
-    out_io.log_tab = c->d_log;
-    out_io.exp_tab = c->d_exp;
-    out_io.mord = c->t.m;
-    out_io.vec = out_io.vec && lg_k > 0 && (reinterpret_cast<uintptr_t>(rx) % 16 == 0) &&
-                 (stride_in % 8 == 0);
-    LCH_TRY((run_plan<R, P>(c, plan_passes(b, lgo, false, true), lgo, batch, nullptr, t, &out_io, t, s)));
-    if (lg_k == 0)
-      return cu(cudaMemcpy2DAsync(out, size_t(stride_out) * 2, tmp, 16, 2, size_t(batch),
-                                  cudaMemcpyDeviceToDevice, s));
-    return LCH_OK;
-  });
+int lch_encode_k(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
+                 int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len, void *stream) {
+  return encode_any(c, msg, stride_in, parity, stride_out, batch, k, packet_len, stream);
 }
 
 int lch_decode(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t *bits, int shared,
                uint16_t *out, int64_t stride_out, int64_t batch, int lg_k, int64_t packet_len,
                const int64_t *host_counts, void *stream) {
-  if (!c || batch < 0 || lg_k < 0 || lg_k > c->t.r || !bits) return LCH_EINVAL;
+  if (!c || lg_k < 0 || lg_k > c->t.r) return LCH_EINVAL;
   if (lg_k > c->max_lg_h) return LCH_EINVAL;
-  if (packet_len != 0) return LCH_EUNSUPPORTED;
-  const int r = c->t.r;
-  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k;
-  if (stride_in < n || stride_out < k) return LCH_EINVAL;
-  LCH_TRY(ensure_device(c));
-  if (batch == 0) return LCH_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!shared) return decode_per_codeword(c, rx, stride_in, bits, out, stride_out, batch, lg_k,
-                                          host_counts, s);
-  int64_t count = 0;
-  if (host_counts) {
-    count = host_counts[0];
-  } else {
-    Scratch sc(s);
-    int64_t *dcount = nullptr;
-    LCH_TRY(sc.alloc(dcount, 1));
-    LCH_TRY(cu(launch_count_bits(bits, 1, int(n / 32 > 0 ? n / 32 : 1), dcount, s)));
-    c->launches++;
-    LCH_TRY(cu(cudaMemcpyAsync(&count, dcount, sizeof(int64_t), cudaMemcpyDeviceToHost, s)));
-    LCH_TRY(cu(cudaStreamSynchronize(s)));
-  }
-  if (count == 0)  // rs.py:119-120
-    return cu(cudaMemcpy2DAsync(out, size_t(stride_out) * 2, rx, size_t(stride_in) * 2, size_t(k) * 2,
-                                size_t(batch), cudaMemcpyDeviceToDevice, s));
-  if (count > n - k) return LCH_ETOOMANY;  // rs.py:121-123
-  if (c->max_lg_h < r) return LCH_EINVAL;  // n-point transforms (transform.py:63-64)
-  return dispatch(c, [&](auto RC, auto PC) -> int {
-    constexpr int R = decltype(RC)::value;
-    constexpr uint32_t P = decltype(PC)::value;
-    Scratch sc(s);
-    uint16_t *logs = nullptr, *pi_row = nullptr, *pinv = nullptr;
-    LCH_TRY(sc.alloc(logs, size_t(n)));
-    LCH_TRY(sc.alloc(pi_row, size_t(n)));
-    LCH_TRY(sc.alloc(pinv, size_t(k)));
-    // rs.py:125 locator values for the shared pattern
-    LCH_TRY(locator_impl(c, bits, 1, nullptr, logs, s));
-    LCH_TRY(cu(launch_decode_rows(logs, bits, c->d_exp, c->t.m, uint32_t(n), uint32_t(k), pi_row,
-                                  pinv, s)));
-    c->launches++;
-    const int lgk_out = std::max(lg_k, 1);
-    uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
-    LCH_TRY(sc.alloc(x, bs_bytes(R, batch, r) / 16));
-    LCH_TRY(sc.alloc(t, bs_bytes(R, batch, lgk_out) / 16));
-    LCH_TRY(sc.alloc(t1, bs_bytes(R, batch, lgk_out) / 16));
-    RawIO in_io = make_raw(const_cast<uint16_t *>(rx), stride_in);
-    // rs.py:130-136: phi = received * Pi_bar and the n-point inverse.  The top
-    // level r-1 is a pure XOR at shift 0 (its only block has factor 0) and is
-    // folded into the derivative below: with x the state after levels
-    // 0..r-2 and y_j = B_(j mod n/2) x_j, the derivative gather of
-    // derivative.py:56-70 for j < k is
-    //   T_j = W'_(r-1) (y_j + y_(j+n/2)) + sum_(l < r-1, bit l of j clear) y_(j | 2^l).
-    std::vector<LOp> a = {{OP_SCALE, 0, 0, pi_row}};
-    for (int i = 0; i + 1 < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
-    a.push_back({OP_SCALE, 0, 0, c->d_b_lo});
-    auto plan_a = plan_passes(a, r, true, false);
-    // the last inverse pass also sums the gather over its own tile bits
-    LCH_TRY((run_plan<R, P>(c, plan_a, r, batch, &in_io, nullptr, nullptr, x, s, t1, lgk_out)));
-    std::vector<int> rest;
-    for (int b = 0; b + 1 < r; ++b)
-      if (std::find(plan_a.back().bits.begin(), plan_a.back().bits.end(), b) == plan_a.back().bits.end())
-        rest.push_back(b);
-    rest.push_back(r - 1);
-    LCH_TRY((run_gather<R, P>(c, x, t, r, lgk_out, batch, rest, r - 1, c->t.w_prime[r - 1], t1, s)));
-    // rs.py:137-148: B^-1 scaling, k-point forward (the first k evaluations of
-    // the n-point forward), division by Pi' on erased positions, survivors copied
-    std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
-    for (int i = lg_k - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
-    if (lg_k == 0) {
-      // 1-point forward = identity; produce 2 columns into a temp, keep column 0
-      uint16_t *tmp = nullptr;
-      LCH_TRY(sc.alloc(tmp, size_t(batch) * 8));
-      uint16_t *pinv2 = nullptr;
-      LCH_TRY(sc.alloc(pinv2, 2));
-      LCH_TRY(cu(cudaMemsetAsync(pinv2, 0, 4, s)));
-      LCH_TRY(cu(cudaMemcpyAsync(pinv2, pinv, 2, cudaMemcpyDeviceToDevice, s)));
-      b.push_back({OP_SCALE, 0, 0, pinv2});
-      RawIO out_io = make_raw(tmp, 8);
-      out_io.merge_src = rx;
-      out_io.merge_stride = stride_in;
-      out_io.merge_bits = bits;
-      out_io.vec = 0;
-      LCH_TRY((run_plan<R, P>(c, plan_passes(b, 1, false, true), 1, batch, nullptr, t, &out_io, t, s)));
-      return cu(cudaMemcpy2DAsync(out, size_t(stride_out) * 2, tmp, 16, 2, size_t(batch),
-                                  cudaMemcpyDeviceToDevice, s));
-    }
-    b.push_back({OP_SCALE, 0, 0, pinv});
-    RawIO out_io = make_raw(out, stride_out);
-    out_io.merge_src = rx;
-    out_io.merge_stride = stride_in;
-    out_io.merge_bits = bits;
-    out_io.vec = out_io.vec && (reinterpret_cast<uintptr_t>(rx) % 16 == 0) && (stride_in % 8 == 0);
-    return run_plan<R, P>(c, plan_passes(b, lg_k, false, true), lg_k, batch, nullptr, t, &out_io, t, s);
-  });
+  return decode_any(c, rx, stride_in, bits, shared, out, stride_out, batch, int64_t(1) << lg_k,
+                    packet_len, host_counts, stream);
+}
+
+int lch_decode_k(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32_t *bits, int shared,
+                 uint16_t *out, int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len,
+                 const int64_t *host_counts, void *stream) {
+  return decode_any(c, rx, stride_in, bits, shared, out, stride_out, batch, k, packet_len, host_counts,
+                    stream);
+}
+
+int lch_set_scratch_limit(lch_ctx *c, uint64_t bytes) {
+  if (!c || bytes == 0) return LCH_EINVAL;
+  c->scratch_limit = size_t(bytes);
+  return LCH_OK;
 }
 
 int lch_gen_symbols(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len, uint16_t *out,
@@ -842,6 +1038,16 @@ int lch_gen_symbols(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int6
   if (batch == 0 || len == 0) return LCH_OK;
   c->launches++;
   return cu(launch_gen_symbols(seed, cw0, batch, len, c->t.m, out, stride,
+                               static_cast<cudaStream_t>(stream)));
+}
+
+int lch_gen_packets(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len, uint16_t *out,
+                    int64_t n_pos, int64_t packet_len, void *stream) {
+  if (!c || batch < 0 || len < 0 || n_pos < len || packet_len <= 0 || batch % packet_len) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || len == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_gen_packets(seed, cw0, batch, len, c->t.m, out, n_pos, packet_len,
                                static_cast<cudaStream_t>(stream)));
 }
 

@@ -197,7 +197,11 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
   const int64_t row0 = int64_t(g) * GROUP;
   const RawIO &io = p.raw_in;
   const bool inwin = int64_t(base) >= io.pos_lo && int64_t(base) + TP <= io.pos_hi;
-  if (io.pkt && inwin) {
+  if (int64_t(base) + TP <= io.pos_lo || int64_t(base) >= io.pos_hi) {
+    // tile entirely outside the input window: zeros
+    uint4 *z = smem;
+    for (int idx = threadIdx.x; idx < WPR * (GROUP / 4); idx += NT) z[idx] = make_uint4(0u, 0u, 0u, 0u);
+  } else if (io.pkt && inwin) {
     // packet-major: 1024 consecutive symbols per position; a thread takes 8
     // rows of one word column (positions 2cw, 2cw+1) and interleaves them
     for (int idx = threadIdx.x; idx < WPR * (GROUP / 8); idx += NT) {
@@ -282,6 +286,7 @@ template <int R>
 __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem, int g,
                                                uint32_t base, int TP) {
   if (p.dbg & 5) return;
+  if (int64_t(base) + TP <= p.raw_out.pos_lo || int64_t(base) >= p.raw_out.pos_hi) return;
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
   const uint4 *bs = smem + bs_offset_u4<R>();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -837,11 +842,17 @@ __global__ void fwht_kernel(const __grid_constant__ FwhtParams p) {
   }
 }
 
-// decode rows from the locator logs: pi_row[j] = erased ? 0 : exp[x],
-// pinv[j] = (erased && j < k) ? exp[(m - x) % m] : 0   (rs.py:130-148)
+// decode rows from the locator logs, one row set per pattern (blockIdx.y):
+// pi_row[j] = erased ? 0 : exp[x], pinv[j] = (erased && j < k) ? exp[(m - x) % m] : 0
+// (rs.py:130-148)
 __global__ void decode_rows_kernel(const uint16_t *logs, const uint32_t *bits,
                                    const uint16_t *exp, uint32_t m, uint32_t n, uint32_t k,
                                    uint16_t *pi_row, uint16_t *pinv) {
+  const size_t pat = blockIdx.y, words = (n + 31) / 32;
+  logs += pat * n;
+  bits += pat * words;
+  pi_row += pat * n;
+  pinv += pat * k;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const uint32_t x = logs[j];
     const bool erased = (bits[j >> 5] >> (j & 31)) & 1u;
@@ -858,6 +869,20 @@ __device__ __forceinline__ uint64_t mix64_d(uint64_t z) {
 __device__ __forceinline__ uint64_t key_d(uint64_t seed, uint64_t cw, uint64_t pos) {
   const uint64_t s = mix64_d(seed + 0x9E3779B97F4A7C15ull);
   return mix64_d(s + ((cw << 32) | pos) * 0x9E3779B97F4A7C15ull);
+}
+
+// packet-major: element index i -> (group, position, packet offset), the
+// packet offset fastest so stores coalesce
+__global__ void gen_packets_kernel(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
+                                   uint32_t mask, uint16_t *out, int64_t npos, int64_t pkt) {
+  const int64_t total = batch * len;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t sidx = i % pkt, rest = i / pkt;
+    const int64_t j = rest % len, g = rest / len;
+    const int64_t b = g * pkt + sidx;
+    out[(g * npos + j) * pkt + sidx] = uint16_t(key_d(seed, cw0 + uint64_t(b), uint64_t(j)) & mask);
+  }
 }
 
 __global__ void gen_symbols_kernel(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
@@ -956,8 +981,9 @@ cudaError_t launch_fwht(const FwhtParams &p, cudaStream_t s) {
 
 cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const uint16_t *exp,
                                uint32_t m, uint32_t n, uint32_t k, uint16_t *pi_row,
-                               uint16_t *pinv, cudaStream_t s) {
-  decode_rows_kernel<<<(n + 255) / 256, 256, 0, s>>>(logs, bits, exp, m, n, k, pi_row, pinv);
+                               uint16_t *pinv, int64_t np, cudaStream_t s) {
+  decode_rows_kernel<<<dim3((n + 255) / 256, unsigned(np)), 256, 0, s>>>(logs, bits, exp, m, n, k,
+                                                                         pi_row, pinv);
   return cudaGetLastError();
 }
 
@@ -967,6 +993,15 @@ cudaError_t launch_gen_symbols(uint64_t seed, uint64_t cw0, int64_t batch, int64
   const int64_t total = batch * len;
   const int blocks = int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
   gen_symbols_kernel<<<blocks, 256, 0, s>>>(seed, cw0, batch, len, mask, out, row_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_packets(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
+                               uint32_t mask, uint16_t *out, int64_t npos, int64_t pkt,
+                               cudaStream_t s) {
+  const int64_t total = batch * len;
+  const int blocks = int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
+  gen_packets_kernel<<<blocks, 256, 0, s>>>(seed, cw0, batch, len, mask, out, npos, pkt);
   return cudaGetLastError();
 }
 

@@ -143,7 +143,10 @@ cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s);
 cudaError_t launch_fwht(const FwhtParams &p, cudaStream_t s);
 cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const uint16_t *exp,
                                uint32_t m, uint32_t n, uint32_t k, uint16_t *pi_row,
-                               uint16_t *pinv, cudaStream_t s);
+                               uint16_t *pinv, int64_t np, cudaStream_t s);
+cudaError_t launch_gen_packets(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
+                               uint32_t mask, uint16_t *out, int64_t npos, int64_t pkt,
+                               cudaStream_t s);
 cudaError_t launch_gen_symbols(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
                                uint32_t mask, uint16_t *out, int64_t row_stride,
                                cudaStream_t s);

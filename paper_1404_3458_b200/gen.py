@@ -22,6 +22,18 @@ def symbols(ctx, seed: int, cw0: int, batch: int, length: int):
     return t
 
 
+def packets(ctx, seed: int, cw0: int, groups: int, length: int, packet_len: int):
+    """[groups, length, P] packet-major symbols; lane g * P + s = codeword cw0 + g * P + s,
+    so lane s of group g equals row g * P + s of `symbols`."""
+    torch = _lib.torch_mod()
+    t = torch.empty((groups, length, packet_len), dtype=torch.int16, device="cuda")
+    if groups and length:
+        _lib.check(_lib.lib.lch_gen_packets(ctx.handle, seed, cw0, groups * packet_len, length,
+                                            t.data_ptr(), length, packet_len, _lib.stream_ptr()),
+                   "gen_packets")
+    return t
+
+
 def erasure_masks(ctx, seed: int, n: int, count: int, cw0: int, batch: int):
     """Bool tensor [batch, n]: True at erased positions."""
     torch = _lib.torch_mod()

@@ -157,7 +157,48 @@ def make_r8() -> None:
             assert list(enc[row]) == ref_rs.encode(cpk, bt, [int(x) for x in m[row]]).symbols
         out[f"k{k}_msg"] = m
         out[f"k{k}_cw"] = enc
+    # general k (no reference codec): codewords and decodes
+    # composed from the reference's own primitives (locator_values, inverse,
+    # derivative_fast, forward), i.e. rs.decode's algorithm evaluated at every
+    # erased position, with encode = erasure-decode of E = [k, n)
+    for k in (3, 100, 192, 240, 255):
+        msgs, cws, masks, decs = [], [], [], []
+        for cw in range(3):
+            m = gen_symbols(1404345805, 8, cw, k)
+            c = recover_all_ref(ft, bt, 256, m + [0] * (256 - k), list(range(k, 256)))
+            assert c[:k] == m
+            e = gen_erasures(1404345805 ^ 0xE, 256, 256 - k, cw)
+            junk = gen_symbols(1404345805 ^ 0x5A5A, 8, cw, 256)
+            rx = [junk[j] if j in set(e) else c[j] for j in range(256)]
+            dec = recover_all_ref(ft, bt, 256, rx, e)
+            assert dec == c
+            mk = np.zeros(256, np.uint8); mk[e] = 1
+            msgs.append(m); cws.append(c); masks.append(mk); decs.append(rx)
+        out[f"anyk{k}_msg"] = np.asarray(msgs, np.uint16)
+        out[f"anyk{k}_cw"] = np.asarray(cws, np.uint16)
+        out[f"anyk{k}_mask"] = np.asarray(masks, np.uint8)
+        out[f"anyk{k}_rx"] = np.asarray(decs, np.uint16)
+    # power-of-two k: the composition equals rs.encode (fact iii)
+    for k in (2, 32, 128):
+        m = gen_symbols(1404345805, 8, 9, k)
+        assert recover_all_ref(ft, bt, 256, m + [0] * (256 - k), list(range(k, 256))) == \
+            ref_rs.encode(ref_rs.CodeParams(8, k), bt, m).symbols
     np.savez_compressed(os.path.join(HERE, "golden_r8.npz"), **out)
+
+
+def recover_all_ref(ft, bt, n, received, erased):
+    """rs.py:125-148 (locator, phi, n-point inverse, derivative, forward,
+    division by Pi') with the recovered value written at EVERY erased position."""
+    es = set(erased)
+    lv = ref_walsh.locator_values(ft, erased)
+    phi = [0 if j in es else ft.mul(received[j], lv.pi_bar[j]) for j in range(n)]
+    coef = inverse(bt, EvalVec(phi, 0)).data
+    d = derivative_fast(bt, CoeffVec(coef)).data
+    ev = forward(bt, CoeffVec(d), 0).data
+    full = list(received)
+    for j in es:
+        full[j] = ft.div(ev[j], lv.pi_prime[j])
+    return full
 
 
 def make_r16() -> None:
@@ -244,8 +285,39 @@ def make_r16() -> None:
         json.dump(res, fh, indent=1)
 
 
+def make_r16_anyk() -> None:
+    """Storage-stripe rates k/n = 3/4, 15/16 (config 5) at r=16, composed from
+    the reference primitives like make_r8's anyk vectors."""
+    ft = tables_for(16)
+    bt = build_basis_tables(ft, 1 << 16)
+    n = 1 << 16
+    res = []
+    for k in (49152, 61440):
+        m = gen_symbols(1404345805, 16, 0, k)
+        c = recover_all_ref(ft, bt, n, m + [0] * (n - k), list(range(k, n)))
+        assert c[:k] == m
+        e = gen_erasures(1404345805 ^ 0xE, n, n - k, 0)
+        junk = gen_symbols(1404345805 ^ 0x5A5A, 16, 0, n)
+        es = set(e)
+        rx = [junk[j] if j in es else c[j] for j in range(n)]
+        assert recover_all_ref(ft, bt, n, rx, e)[:k] == m
+        jd = recover_all_ref(ft, bt, n, junk, e)[:k]
+        res.append(dict(k=k, seed=1404345805, cw=0, parity=dict(sha256=digest(c[k:]), sample=sample(c[k:])),
+                        erasure_seed=1404345805 ^ 0xE, junk_seed=1404345805 ^ 0x5A5A,
+                        pattern_sha256=digest(np.asarray(e, np.uint32)),
+                        junk_out=dict(sha256=digest(jd), sample=sample(jd))))
+    with open(os.path.join(HERE, "golden_r16_anyk.json"), "w") as f:
+        json.dump(res, f, indent=1)
+
+
 if __name__ == "__main__":
-    make_r8()
-    print("r8 done", flush=True)
-    make_r16()
-    print("r16 done", flush=True)
+    which = sys.argv[1:] or ["r8", "r16"]
+    if "r8" in which:
+        make_r8()
+        print("r8 done", flush=True)
+    if "r16" in which:
+        make_r16()
+        print("r16 done", flush=True)
+    if "r16" in which or "r16_anyk" in which:
+        make_r16_anyk()
+        print("r16_anyk done", flush=True)

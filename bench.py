@@ -1,12 +1,13 @@
 #!/usr/bin/env python3
 """Benchmark: RS(2^16, 2^15) GF(2^16) encode + erasure-decode on B200.
 
-One step = encode 4096 codewords (config 3: 256 MiB of uint16 message, parity
-written separately) + erasure-decode 4096 codewords with one shared pattern of
-2^15 erased positions (config 4a), per GPU.  Multi-GPU is weak scaling: rank
-r owns codewords [r*4096, (r+1)*4096), no collective on the data
-path; the timed region is bracketed by barrier + synchronize and the reported
-time is the max over ranks.
+Default workload (`--workload codec`, the BASELINE.json headline): one step =
+encode 4096 codewords (config 3: 256 MiB of uint16 message, parity written
+separately) + erasure-decode 4096 codewords with one shared pattern of 2^15
+erased positions (config 4a), per GPU.  Multi-GPU is weak scaling: rank r owns
+codewords [r*4096, (r+1)*4096), no collective on the data path;
+the timed region is bracketed by barrier + synchronize and the reported time
+is the max over ranks.
 
   value      = message bytes encoded + decoded (2 * k * 2 B per codeword, all
                ranks) / max-over-ranks step time, GB/s (1e9)
@@ -16,9 +17,20 @@ time is the max over ranks.
   roofline   = dominant kernel (pass_kernel, the encode's 5 tile passes):
                algorithmic bytes per launch (4 B per symbol-position: 2 B read +
                2 B write, SURVEY §8d "transform pass: 4h bytes per polynomial")
-               / average launch duration, vs measured HBM copy bandwidth
+               / average launch duration (CUDA events on the launch stream), vs
+               measured HBM copy bandwidth
   cpu_baseline = the C oracle (restated reference algorithm) on the host cores,
                rank 0, bounded sample
+
+Other §8 rows (auxiliary lines, same JSON keys):
+  --workload stripe --rate 1/2|3/4|15/16   config 5: 4 KiB packets, 32 GiB of
+               message split over the GPUs (strong scaling), per-stripe-group
+               erasure patterns of n-k packets
+  --workload transform                     config 2: forward + inverse +
+               derivative, h = 2^16, 1024 polynomials per GPU
+  --workload pcw                           config 4b: decode 4096 codewords with
+               per-codeword patterns
+  --workload r8                            config 1: (256,128), 64 codewords
 
 `--impl reference` times the reference's CPU path (oracle port, all host
 threads) on the same config and prints the reference-arm JSON line.
@@ -39,18 +51,17 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_1404_3458_b200.dist import env_rank  # noqa: E402
+
 R_BITS, N, K = 16, 1 << 16, 1 << 15
 BATCH = 4096
 SEED_MSG, SEED_ERA = 1404345803, 1404345804
+SEED_CFG = {1: 1404345801, 2: 1404345802, 5: 1404345805}
 METRIC = "RS(2^16,2^15) GF(2^16) encode & erasure-decode GB/s; % of HBM roofline"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-
-
-def env_rank():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+STRIPE = {"1/2": (1 << 15, 256), "3/4": (49152, 168), "15/16": (61440, 136)}  # k, groups
+PKT = 2048
+DATA = "synthetic (seeded counter-based generator, SURVEY §8d)"
 
 
 def hbm_peak():
@@ -120,8 +131,11 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_reference(sample_cw: int, nthreads: int):
-    """Time the oracle (restated reference) encode + shared-pattern decode."""
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = restated reference; bounded samples)
+
+def cpu_codec(sample_cw: int, nthreads: int):
+    """Time the oracle encode + shared-pattern decode (configs 3 + 4a)."""
     from oracle import oracle as O
     orc = O.Oracle(16)
     msgs = O.gen_symbols(SEED_MSG, 16, 0, sample_cw, K)
@@ -143,61 +157,202 @@ def cpu_reference(sample_cw: int, nthreads: int):
             "encode_s": round(t1 - t0, 3), "decode_s": round(t3 - t2, 3)}
 
 
+def cpu_stripe(k: int, lanes: int, nthreads: int):
+    """Config 5 lanes (one lane = one codeword) through the general-k oracle."""
+    from oracle import oracle as O
+    orc = O.Oracle(16)
+    msgs = O.gen_symbols(SEED_CFG[5], 16, 0, lanes, k)
+    mask = O.gen_erasures(SEED_CFG[5] ^ 0xE, N, N - k, 0, 1)[0]
+    t0 = time.perf_counter()
+    par = orc.encode_any_batch(k, msgs, nthreads)
+    t1 = time.perf_counter()
+    rx = np.concatenate([msgs, par], axis=1)
+    rx[:, mask == 1] = 0
+    t2 = time.perf_counter()
+    out = orc.decode_any_batch(k, rx, mask, nthreads)
+    t3 = time.perf_counter()
+    assert np.array_equal(out, msgs), "oracle round trip failed"
+    sec = (t1 - t0) + (t3 - t2)
+    return {"value": round(lanes * 2 * k * 2 / sec / 1e9, 6), "unit": "GB/s", "cores": nthreads,
+            "kind": "port",
+            "sample": f"{lanes} packet lanes (codewords) of RS(2^16,{k}) encode + decode with "
+                      f"{N - k} erasures, C oracle, {nthreads} threads"}
+
+
+def cpu_transform(polys: int, nthreads: int):
+    from oracle import oracle as O
+    orc = O.Oracle(16)
+    a = O.gen_symbols(SEED_CFG[2], 16, 0, polys, N)
+    t0 = time.perf_counter()
+    orc.transform_batch(a, 0, False, nthreads)
+    orc.transform_batch(a, 0, True, nthreads)
+    for b in range(polys):
+        orc.derivative(a[b])
+    sec = time.perf_counter() - t0
+    return {"value": round(3 * polys * 4 * N / sec / 1e9, 6), "unit": "GB/s", "cores": nthreads,
+            "kind": "port",
+            "sample": f"{polys} polynomials h=2^16 forward + inverse ({nthreads} threads) + "
+                      "derivative (1 thread), C oracle"}
+
+
+def cpu_pcw(cws: int, nthreads: int):
+    from oracle import oracle as O
+    orc = O.Oracle(16)
+    msgs = O.gen_symbols(SEED_MSG, 16, 0, cws, K)
+    masks = O.gen_erasures(SEED_ERA, N, N - K, 0, cws)
+    par = orc.encode_batch(K, msgs, nthreads)
+    rx = np.concatenate([msgs, par], axis=1)
+    rx[masks == 1] = 0
+    t0 = time.perf_counter()
+    out = orc.decode_batch(K, rx, masks, nthreads)
+    sec = time.perf_counter() - t0
+    assert np.array_equal(out, msgs)
+    return {"value": round(cws * K * 2 / sec / 1e9, 6), "unit": "GB/s", "cores": nthreads,
+            "kind": "port",
+            "sample": f"{cws} per-codeword-pattern decodes RS(2^16,2^15), C oracle, {nthreads} threads"}
+
+
+def cpu_r8(nthreads: int):
+    from oracle import oracle as O
+    orc = O.Oracle(8)
+    msgs = O.gen_symbols(SEED_CFG[1], 8, 0, 64, 128)
+    masks = O.gen_erasures(SEED_CFG[1] ^ 0xE, 256, 128, 0, 64)
+    reps = 20
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        par = orc.encode_batch(128, msgs, 1)
+        rx = np.concatenate([msgs, par], axis=1)
+        out = orc.decode_batch(128, rx, masks, 1)
+    sec = (time.perf_counter() - t0) / reps
+    assert np.array_equal(out, msgs)
+    return {"value": round(2 * 64 * 128 / sec / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": "64 codewords (256,128) encode + per-codeword decode, C oracle, 1 thread"}
+
+
+# ---------------------------------------------------------------------------
+
 def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
     nth = cpu_threads()
-    sample = max(nth, 16)
-    vals = []
-    for _ in range(max(args.warmup, 0) and 1):
-        cpu_reference(min(sample, 16), nth)
-    for _ in range(args.steps):
-        vals.append(cpu_reference(sample, nth))
+    wl = args.workload
+    if wl == "codec":
+        sample = max(nth, 16)
+        cpu_codec(min(sample, 16), nth)
+        vals = [cpu_codec(sample, nth) for _ in range(args.steps)]
+        unit_bytes = BATCH * 2 * K * 2
+        cfg = {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern decode "
+                           "4096 cw (2^15 erasures) per GPU; CPU arm times a "
+                           f"{sample}-codeword sample and extrapolates the rate",
+               "batch_per_gpu": BATCH, "n": N, "k": K}
+    elif wl == "stripe":
+        k, groups = STRIPE[args.rate]
+        vals = [cpu_stripe(k, max(nth, 16), nth) for _ in range(max(1, min(args.steps, 3)))]
+        unit_bytes = groups * PKT * k * 2 * 2
+        cfg = {"workload": f"cfg5: RS(2^16,{k}) 4 KiB packets, {groups} stripe groups", "k": k}
+    elif wl == "transform":
+        vals = [cpu_transform(max(nth, 8), nth) for _ in range(max(1, min(args.steps, 3)))]
+        unit_bytes = 1024 * 3 * 4 * N
+        cfg = {"workload": "cfg2: forward+inverse+derivative h=2^16 x 1024", "h": N}
+    elif wl == "pcw":
+        vals = [cpu_pcw(max(nth, 16), nth) for _ in range(max(1, min(args.steps, 3)))]
+        unit_bytes = BATCH * K * 2
+        cfg = {"workload": "cfg4b: per-codeword-pattern decode 4096 cw", "n": N, "k": K}
+    else:
+        vals = [cpu_r8(nth) for _ in range(max(1, min(args.steps, 3)))]
+        unit_bytes = 2 * 64 * 128
+        cfg = {"workload": "cfg1: r=8 (256,128) 64 cw encode + per-codeword decode"}
     v = float(np.median([x["value"] for x in vals]))
     cb = dict(vals[-1])
     cb["value"] = round(v, 6)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(BATCH * 2 * K * 2 / (v * 1e9) * 1e3, 3),
+            "ms_per_step": round(unit_bytes / (v * 1e9) * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
-            "data": "synthetic (seeded counter-based generator, SURVEY §8d)",
-            "config": {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern "
-                                   "decode 4096 cw (2^15 erasures) per GPU; CPU arm times a "
-                                   f"{sample}-codeword sample and extrapolates the rate",
-                       "batch_per_gpu": BATCH, "n": N, "k": K},
-            "cpu_baseline": cb,
+            "data": DATA, "config": cfg, "cpu_baseline": cb,
             "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="lch", choices=["lch", "reference"])
-    ap.add_argument("--batch", type=int, default=BATCH)
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--only", default="", help="encode|decode (profiling runs)")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference_arm(args)
+class Timer:
+    """Per-phase CUDA-event timing of `steps` steps on the launch stream."""
 
-    import torch
-    import torch.distributed as dist
+    def __init__(self, torch, stream):
+        self.torch, self.stream = torch, stream
 
-    rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    import paper_1404_3458_b200 as lch
-    from paper_1404_3458_b200 import _lib
+    def ev(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def run(self, phases, steps, warmup, world, local, lib, ctx):
+        torch, dist = self.torch, None
+        if world > 1:
+            import torch.distributed as dist
+        for _ in range(warmup):
+            for _, fn in phases:
+                fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        n0 = lib.lch_launch_count(ctx)
+        marks = []
+        with ClockSampler(local) as clk:
+            t0 = self.ev()
+            t0.record(self.stream)
+            for _ in range(steps):
+                evs = [self.ev() for _ in range(len(phases) + 1)]
+                evs[0].record(self.stream)
+                for i, (_, fn) in enumerate(phases):
+                    fn()
+                    evs[i + 1].record(self.stream)
+                marks.append(evs)
+            t1 = self.ev()
+            t1.record(self.stream)
+            torch.cuda.synchronize()
+        launches = lib.lch_launch_count(ctx) - n0
+        step_ms = t0.elapsed_time(t1) / steps
+        ph = [float(np.mean([m[i].elapsed_time(m[i + 1]) for m in marks])) for i in range(len(phases))]
+        if world > 1:
+            t = torch.tensor([step_ms] + ph, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            vals = [float(x) for x in t.tolist()]
+            step_ms, ph = vals[0], vals[1:]
+        return step_ms, dict(zip([n for n, _ in phases], ph)), int(launches), clk.summary()
+
+
+def read_traffic():
+    tfile = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            with open(tfile) as fh:
+                return json.load(fh).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def base_line(args, world, value, step_ms, cfg, launches, clocks, scaling="weak"):
+    return {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "u16",
+            "data": DATA, "config": cfg, "gpu_launches": launches, "clocks": clocks}
+
+
+def roofline(name, alg_bytes, ms, peak, peak_src, traffic=None):
+    ach = alg_bytes / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": name, "achieved": round(ach, 2), "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": round(ach / peak, 4),
+            "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+            "avg_launch_ms": round(ms, 4)}
+
+
+# ---------------------------------------------------------------------------
+
+def run_codec(args, torch, lch, _lib, world, rank, local):
+    from paper_1404_3458_b200 import gen
     from paper_1404_3458_b200.rs import decode_device, encode_device
-
     B = args.batch
     ft = lch.tables_for(16)
     bt = lch.build_basis_tables(ft, N)
@@ -213,7 +368,6 @@ def main():
     cw = torch.empty((B, N), dtype=torch.int16, device="cuda")
     cw[:, :K].copy_(msg)
     parity = cw[:, K:]
-    from paper_1404_3458_b200 import gen
     emask = gen.erasure_masks(bt.ctx, SEED_ERA, N, N - K, 0, 1)  # shared pattern (cw index 0)
     bits = gen.mask_to_bits(emask)[0].contiguous()
     out = torch.empty((B, K), dtype=torch.int16, device="cuda")
@@ -231,95 +385,44 @@ def main():
     rx[:, era_cols] = 0
     decode_device(cp, bt, rx, bits, out, N - K)
     torch.cuda.synchronize()
-    ok = bool(torch.equal(out, msg))
-    if not ok:
+    if not bool(torch.equal(out, msg)):
         print(json.dumps({"error": "round trip failed", "rank": rank}), flush=True)
-        return 1
+        return None
 
-    do_enc = args.only in ("", "encode")
-    do_dec = args.only in ("", "decode")
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    for _ in range(args.warmup):
-        if do_enc:
-            step_encode()
-        if do_dec:
-            step_decode()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    n0 = _lib.lib.lch_launch_count(ctx)
-    enc_ms, dec_ms = [], []
-    with ClockSampler(local) as clk:
-        t_start = ev()
-        t_start.record(stream)
-        for _ in range(args.steps):
-            e0, e1, e2 = ev(), ev(), ev()
-            e0.record(stream)
-            if do_enc:
-                step_encode()
-            e1.record(stream)
-            if do_dec:
-                step_decode()
-            e2.record(stream)
-            enc_ms.append((e0, e1))
-            dec_ms.append((e1, e2))
-        t_end = ev()
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    launches = _lib.lib.lch_launch_count(ctx) - n0
-    total_ms = t_start.elapsed_time(t_end)
-    enc = float(np.mean([a.elapsed_time(b) for a, b in enc_ms]))
-    dec = float(np.mean([a.elapsed_time(b) for a, b in dec_ms]))
-    step_ms = total_ms / args.steps
-    if world > 1:
-        t = torch.tensor([step_ms, enc, dec], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms, enc, dec = (float(x) for x in t.tolist())
-
+    phases = []
+    if args.only in ("", "encode"):
+        phases.append(("encode", step_encode))
+    if args.only in ("", "decode"):
+        phases.append(("decode", step_decode))
+    step_ms, ph, launches, clocks = Timer(torch, stream).run(phases, args.steps, args.warmup, world,
+                                                             local, _lib.lib, ctx)
     msg_bytes = B * K * 2
-    nphases = int(do_enc) + int(do_dec)
-    value = world * nphases * msg_bytes / (step_ms * 1e-3) / 1e9
+    value = world * len(phases) * msg_bytes / (step_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
+    enc, dec = ph.get("encode"), ph.get("decode")
     # dominant kernel: the encode's pass_kernel launches (5 per encode)
-    enc_launches = 5
-    per_launch_ms = enc / enc_launches if do_enc else dec / 8
+    per_launch_ms = enc / 5 if enc else dec / 8
     per_launch_bytes = 4 * K * B  # 2 B read + 2 B write per symbol-position
-    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
-    if os.path.exists(tfile):
-        try:
-            with open(tfile) as fh:
-                traffic = json.load(fh).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
     codec_alg = 2 * N * B  # encode: read k + write n-k symbols (2 B each) per codeword
-    res = {
-        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
-        "data": "synthetic (seeded counter-based generator, SURVEY §8d)",
-        "config": {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern decode "
-                               "4096 cw (2^15 erasures) per GPU",
-                   "batch_per_gpu": B, "n": N, "k": K, "parallelism": f"codeword-shard x{world}",
-                   "l2": "inputs larger than L2 (256 MiB message, 512 MiB received per GPU)"},
-        "encode_ms": round(enc, 4), "decode_ms": round(dec, 4),
-        "encode_gbs": round(world * msg_bytes / (enc * 1e-3) / 1e9, 3) if do_enc else None,
-        "decode_gbs": round(world * msg_bytes / (dec * 1e-3) / 1e9, 3) if do_dec else None,
-        "encode_hbm_frac": round(codec_alg / (enc * 1e-3) / 1e9 / peak, 4) if do_enc else None,
+    cfg = {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern decode "
+                       "4096 cw (2^15 erasures) per GPU",
+           "batch_per_gpu": B, "n": N, "k": K, "parallelism": f"codeword-shard x{world}",
+           "l2": "inputs larger than L2 (256 MiB message, 512 MiB received per GPU)"}
+    res = base_line(args, world, value, step_ms, cfg, launches, clocks)
+    res.update({
+        "encode_ms": round(enc, 4) if enc else None, "decode_ms": round(dec, 4) if dec else None,
+        "encode_gbs": round(world * msg_bytes / (enc * 1e-3) / 1e9, 3) if enc else None,
+        "decode_gbs": round(world * msg_bytes / (dec * 1e-3) / 1e9, 3) if dec else None,
+        "encode_hbm_frac": round(codec_alg / (enc * 1e-3) / 1e9 / peak, 4) if enc else None,
         "decode_hbm_frac": round((2 * (N - K) + 2 * K) * B / (dec * 1e-3) / 1e9 / peak, 4)
-        if do_dec else None,
-        "roofline": {"bound": "hbm", "kernel": "pass_kernel<16,0x1100B> (encode tile pass)",
-                     "achieved": round(achieved, 2), "peak": peak, "peak_source": peak_src,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "algorithmic_bytes_per_launch": per_launch_bytes,
-                     "avg_launch_ms": round(per_launch_ms, 4)},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
-    }
+        if dec else None,
+        "roofline": roofline("pass_kernel<16,0x1100B> (encode tile pass)", per_launch_bytes,
+                             per_launch_ms, peak, peak_src, read_traffic()),
+    })
 
     # e2e through the public API with pinned host buffers
     if not args.no_e2e:
+        import torch.distributed as dist
         h_msg = torch.empty((B, K), dtype=torch.int16, pin_memory=True)
         h_msg.copy_(msg.cpu())
         h_par = torch.empty((B, N - K), dtype=torch.int16, pin_memory=True)
@@ -344,7 +447,8 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        a, b = ev(), ev()
+        tm = Timer(torch, stream)
+        a, b = tm.ev(), tm.ev()
         a.record(stream)
         e2e_steps = max(1, min(args.steps, 5))
         for _ in range(e2e_steps):
@@ -361,13 +465,244 @@ def main():
                       "unit": "GB/s", "h2d_bytes_per_step": B * K * 2 + B * N * 2,
                       "d2h_bytes_per_step": B * (N - K) * 2 + B * K * 2,
                       "ms_per_step": round(e2e_ms, 3)}
-
     if rank == 0 and not args.no_cpu:
         nth = cpu_threads()
-        res["cpu_baseline"] = cpu_reference(max(8, min(nth, 64)), nth)
+        res["cpu_baseline"] = cpu_codec(max(8, min(nth, 64)), nth)
+    return res
+
+
+def run_stripe(args, torch, lch, _lib, world, rank, local):
+    """Config 5: codeword buffer [G, n, P] per GPU, message = positions [0, k)."""
+    from paper_1404_3458_b200 import gen
+    from paper_1404_3458_b200.dist import split_range
+    k, groups_total = STRIPE[args.rate]
+    if args.groups:
+        groups_total = args.groups
+    g_lo, g_hi = split_range(rank, world, groups_total)  # strong scaling: 32 GiB total
+    G = g_hi - g_lo
+    bt = lch.build_basis_tables(lch.tables_for(16), N)
+    ctx = bt.ctx.handle
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+    lanes = G * PKT
+    cw = torch.empty((G, N, PKT), dtype=torch.int16, device="cuda")
+    # message packets: lane g * P + t of group g is codeword (g_lo * P + lane)
+    _lib.check(_lib.lib.lch_gen_packets(ctx, SEED_CFG[5], g_lo * PKT, lanes, k, cw.data_ptr(), N,
+                                        PKT, s))
+    out = torch.empty((G, k, PKT), dtype=torch.int16, device="cuda")
+    masks = gen.erasure_masks(bt.ctx, SEED_CFG[5] ^ 0xE, N, N - k, g_lo, G)  # one per group
+    bits = gen.mask_to_bits(masks).contiguous()
+    counts = (torch.full((G,), N - k, dtype=torch.int64)).numpy()
+    import ctypes
+    cnt = (ctypes.c_int64 * G)(*[int(x) for x in counts])
+    par_ptr = cw.data_ptr() + k * PKT * 2
+
+    def step_encode():
+        _lib.check(_lib.lib.lch_encode_k(ctx, cw.data_ptr(), N, par_ptr, N, lanes, k, PKT, s))
+
+    def step_decode():
+        _lib.check(_lib.lib.lch_decode_k(ctx, cw.data_ptr(), N, bits.data_ptr(), 0, out.data_ptr(), k,
+                                         lanes, k, PKT, cnt, s))
+
+    step_encode()
+    step_decode()
+    torch.cuda.synchronize()
+    if not bool(torch.equal(out, cw[:, :k, :])):
+        print(json.dumps({"error": "stripe round trip failed", "rank": rank}), flush=True)
+        return None
+    phases = [("encode", step_encode), ("decode", step_decode)]
+    step_ms, ph, launches, clocks = Timer(torch, stream).run(phases, args.steps, args.warmup, world,
+                                                             local, _lib.lib, ctx)
+    msg_bytes = lanes * k * 2
+    total_msg = groups_total * PKT * k * 2
+    value = 2 * total_msg / (step_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    enc, dec = ph["encode"], ph["decode"]
+    cfg = {"workload": f"cfg5: storage stripes RS(2^16,{k}) (k/n={args.rate}), 4 KiB packets "
+                       f"(P={PKT}), {groups_total} stripe groups = {total_msg / 2**30:.1f} GiB of "
+                       "message over all GPUs; encode + decode with per-group patterns of n-k "
+                       "erased packets",
+           "k": k, "n": N, "packet_len": PKT, "groups_total": groups_total,
+           "groups_per_gpu": G, "parallelism": f"stripe-group shard x{world}",
+           "l2": "inputs larger than L2"}
+    res = base_line(args, world, value, step_ms, cfg, launches, clocks, scaling="strong")
+    res.update({
+        "encode_ms": round(enc, 3), "decode_ms": round(dec, 3),
+        "encode_gbs": round(world * msg_bytes / (enc * 1e-3) / 1e9, 3),
+        "decode_gbs": round(world * msg_bytes / (dec * 1e-3) / 1e9, 3),
+        "encode_hbm_frac": round(lanes * 2 * N / (enc * 1e-3) / 1e9 / peak, 4),
+        "decode_hbm_frac": round(lanes * 2 * N / (dec * 1e-3) / 1e9 / peak, 4),
+        "roofline": roofline("encode (whole pipeline, algorithmic 2n B per lane)", lanes * 2 * N, enc,
+                             peak, peak_src),
+        "e2e": None,
+    })
+    if rank == 0 and not args.no_cpu:
+        nth = cpu_threads()
+        res["cpu_baseline"] = cpu_stripe(k, max(8, min(nth, 64)), nth)
+    return res
+
+
+def run_transform_wl(args, torch, lch, _lib, world, rank, local):
+    """Config 2: forward + inverse + derivative, h = 2^16, 1024 polynomials per GPU."""
+    from paper_1404_3458_b200.derivative import run_derivative
+    from paper_1404_3458_b200.transform import run_transform
+    B = 1024
+    bt = lch.build_basis_tables(lch.tables_for(16), N)
+    ctx = bt.ctx.handle
+    stream = torch.cuda.current_stream()
+    a = torch.empty((B, N), dtype=torch.int16, device="cuda")
+    _lib.check(_lib.lib.lch_gen_symbols(ctx, SEED_CFG[2], rank * B, B, N, a.data_ptr(), N,
+                                        stream.cuda_stream))
+    a0 = a.clone()
+    d = torch.empty_like(a)
+    run_transform(bt, a, 0, False)
+    run_transform(bt, a, 0, True)
+    torch.cuda.synchronize()
+    if not bool(torch.equal(a, a0)):
+        print(json.dumps({"error": "transform round trip failed"}), flush=True)
+        return None
+    phases = [("forward", lambda: run_transform(bt, a, 0, False)),
+              ("inverse", lambda: run_transform(bt, a, 0, True)),
+              ("derivative", lambda: run_derivative(bt, a, d))]
+    step_ms, ph, launches, clocks = Timer(torch, stream).run(phases, args.steps, args.warmup, world,
+                                                             local, _lib.lib, ctx)
+    per = 4 * N * B  # 4h bytes per polynomial per pass (SURVEY §8d)
+    value = world * 3 * per / (step_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    cfg = {"workload": "cfg2: forward + inverse + derivative, h=2^16, 1024 polynomials per GPU",
+           "h": N, "batch_per_gpu": B, "parallelism": f"polynomial-shard x{world}"}
+    res = base_line(args, world, value, step_ms, cfg, launches, clocks)
+    res.update({f"{k}_ms": round(v, 4) for k, v in ph.items()})
+    res.update({f"{k}_gbs": round(world * per / (v * 1e-3) / 1e9, 2) for k, v in ph.items()})
+    res["roofline"] = roofline("forward transform (4 passes)", per, ph["forward"], peak, peak_src)
+    res["e2e"] = None
+    if rank == 0 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_transform(max(8, cpu_threads()), cpu_threads())
+    return res
+
+
+def run_pcw(args, torch, lch, _lib, world, rank, local):
+    """Config 4b: decode 4096 codewords, one erasure pattern per codeword."""
+    from paper_1404_3458_b200 import gen
+    from paper_1404_3458_b200.rs import decode_device, encode_device
+    B = args.batch
+    bt = lch.build_basis_tables(lch.tables_for(16), N)
+    cp = lch.CodeParams(16, K)
+    ctx = bt.ctx.handle
+    stream = torch.cuda.current_stream()
+    msg = torch.empty((B, K), dtype=torch.int16, device="cuda")
+    _lib.check(_lib.lib.lch_gen_symbols(ctx, SEED_MSG, rank * B, B, K, msg.data_ptr(), K,
+                                        stream.cuda_stream))
+    cw = torch.empty((B, N), dtype=torch.int16, device="cuda")
+    cw[:, :K].copy_(msg)
+    encode_device(cp, bt, msg, cw[:, K:])
+    masks = gen.erasure_masks(bt.ctx, SEED_ERA, N, N - K, rank * B, B)
+    bits = gen.mask_to_bits(masks).contiguous()
+    cw[masks] = 0
+    out = torch.empty((B, K), dtype=torch.int16, device="cuda")
+    counts = [N - K] * B
+    step = lambda: decode_device(cp, bt, cw, bits, out, counts)  # noqa: E731
+    step()
+    torch.cuda.synchronize()
+    if not bool(torch.equal(out, msg)):
+        print(json.dumps({"error": "pcw round trip failed"}), flush=True)
+        return None
+    step_ms, ph, launches, clocks = Timer(torch, stream).run([("decode", step)], args.steps,
+                                                             args.warmup, world, local, _lib.lib, ctx)
+    value = world * B * K * 2 / (step_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    cfg = {"workload": "cfg4b: RS(2^16,2^15) decode 4096 cw, per-codeword patterns of 2^15 erasures",
+           "batch_per_gpu": B, "n": N, "k": K, "parallelism": f"codeword-shard x{world}"}
+    res = base_line(args, world, value, step_ms, cfg, launches, clocks)
+    alg = (2 * K + 2 * K + N // 8) * B
+    res["roofline"] = roofline("decode pipeline (algorithmic: survivors + output + bitmask)", alg,
+                               ph["decode"], peak, peak_src)
+    res["e2e"] = None
+    if rank == 0 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_pcw(max(8, min(cpu_threads(), 32)), cpu_threads())
+    return res
+
+
+def run_r8(args, torch, lch, _lib, world, rank, local):
+    """Config 1: GF(2^8) (256,128), 64 codewords, 128 per-codeword erasures."""
+    from paper_1404_3458_b200 import gen
+    from paper_1404_3458_b200.rs import decode_device, encode_device
+    B, n, k = 64, 256, 128
+    bt = lch.build_basis_tables(lch.tables_for(8), n)
+    cp = lch.CodeParams(8, k)
+    ctx = bt.ctx.handle
+    stream = torch.cuda.current_stream()
+    msg = gen.symbols(bt.ctx, SEED_CFG[1], rank * B, B, k)
+    cw = torch.empty((B, n), dtype=torch.int16, device="cuda")
+    cw[:, :k].copy_(msg)
+    masks = gen.erasure_masks(bt.ctx, SEED_CFG[1] ^ 0xE, n, n - k, rank * B, B)
+    bits = gen.mask_to_bits(masks).contiguous()
+    out = torch.empty((B, k), dtype=torch.int16, device="cuda")
+    counts = [n - k] * B
+
+    def step_enc():
+        encode_device(cp, bt, msg, cw[:, k:])
+
+    def step_dec():
+        decode_device(cp, bt, cw, bits, out, counts)
+
+    step_enc()
+    step_dec()
+    torch.cuda.synchronize()
+    if not bool(torch.equal(out, msg)):
+        print(json.dumps({"error": "r8 round trip failed"}), flush=True)
+        return None
+    step_ms, ph, launches, clocks = Timer(torch, stream).run(
+        [("encode", step_enc), ("decode", step_dec)], args.steps, args.warmup, world, local,
+        _lib.lib, ctx)
+    value = world * 2 * B * k / (step_ms * 1e-3) / 1e9
+    peak, peak_src = hbm_peak()
+    cfg = {"workload": "cfg1: GF(2^8) (256,128) encode + per-codeword decode, 64 cw per GPU "
+                       "(launch-latency bound)", "batch_per_gpu": B, "n": n, "k": k}
+    res = base_line(args, world, value, step_ms, cfg, launches, clocks)
+    res.update({"encode_ms": round(ph["encode"], 4), "decode_ms": round(ph["decode"], 4)})
+    res["roofline"] = roofline("encode (latency bound)", 2 * n * B, ph["encode"], peak, peak_src)
+    res["e2e"] = None
+    if rank == 0 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_r8(cpu_threads())
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lch", choices=["lch", "reference"])
+    ap.add_argument("--workload", default="codec", choices=["codec", "stripe", "transform", "pcw", "r8"])
+    ap.add_argument("--rate", default="1/2", choices=sorted(STRIPE))
+    ap.add_argument("--groups", type=int, default=0, help="stripe groups (default: 32 GiB)")
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--only", default="", help="encode|decode (profiling runs)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1404_3458_b200 as lch
+    from paper_1404_3458_b200 import _lib
+
+    fn = {"codec": run_codec, "stripe": run_stripe, "transform": run_transform_wl, "pcw": run_pcw,
+          "r8": run_r8}[args.workload]
+    res = fn(args, torch, lch, _lib, world, rank, local)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if res is None:
+        return 1
     if rank == 0:
         print(json.dumps(res), flush=True)
     return 0

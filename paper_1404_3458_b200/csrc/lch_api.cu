@@ -312,23 +312,49 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
   const int ngroups = int((batch + GROUP - 1) / GROUP);
   std::sort(bits.begin(), bits.end());
   if (special >= 0) bits.erase(std::remove(bits.begin(), bits.end(), special), bits.end());
+  // shared-memory need of a tile over `grp` (+ the special bit), one lane-word
+  auto need = [&](const std::vector<int> &grp, bool first) {
+    int nlow = 0;
+    const int nb = int(grp.size()) + (first && special >= 0 ? 1 : 0);
+    for (int b : grp) nlow += b < lgH_out;
+    const bool has_tin = !first || t_in;
+    return ((size_t(1) << nb) + (has_tin ? (size_t(1) << nlow) : 0)) * R * 4;
+  };
+  // greedy split (largest tiles), then the same number of passes with
+  // balanced sizes so no pass degenerates into tiny tiles
+  auto split = [&](size_t cap) {
+    std::vector<std::vector<int>> out;
+    size_t i = 0;
+    bool first = true;
+    while (i < bits.size()) {
+      std::vector<int> grp;
+      const size_t room = std::min<size_t>(cap, GMAXB - (first && special >= 0 ? 1 : 0));
+      while (i < bits.size() && grp.size() < room) {
+        grp.push_back(bits[i]);
+        if (need(grp, first) > GATHER_SMEM_MAX) {
+          grp.pop_back();
+          break;
+        }
+        ++i;
+      }
+      if (grp.empty()) break;
+      out.push_back(grp);
+      first = false;
+    }
+    return out;
+  };
+  auto groups = split(GMAXB);
+  if (groups.size() > 1) {
+    const size_t per = (bits.size() + groups.size() - 1) / groups.size();
+    auto bal = split(per);
+    if (bal.size() == groups.size()) groups = bal;
+  }
+  if (groups.empty() && special >= 0) groups.push_back({});
   bool first = true;
-  size_t i = 0;
-  do {
+  for (auto grp : groups) {
     GatherParams p;
     std::memset(&p, 0, sizeof(p));
-    std::vector<int> grp;
-    const int room = GMAXB - (first && special >= 0 ? 1 : 0);
-    const bool has_tin = !first || t_in;
-    while (i < bits.size() && int(grp.size()) < room) {
-      // shared-memory budget: y tile (+ T_in at the tile's output positions)
-      int nlow = 0, nb = int(grp.size()) + 1 + (first && special >= 0 ? 1 : 0);
-      for (int b : grp) nlow += b < lgH_out;
-      nlow += bits[i] < lgH_out;
-      const size_t need = ((size_t(1) << nb) + (has_tin ? (size_t(1) << nlow) : 0)) * R * 4;
-      if (need > GATHER_SMEM_MAX) break;
-      grp.push_back(bits[i++]);
-    }
+    const size_t nd = need(grp, first);
     p.sb = -1;
     if (first && special >= 0) {
       grp.push_back(special);
@@ -336,9 +362,10 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
       p.sb = int(std::find(grp.begin(), grp.end(), special) - grp.begin());
       p.c = cconst;
     }
-    if (grp.empty()) break;
     p.nbits = int(grp.size());
-    for (size_t m = 0; m < grp.size(); ++m) p.bits[m] = grp[m];
+    // lane-words per CTA: >= ~2048 position-words per CTA within the smem budget
+    p.lwpc = 0;
+    while (p.lwpc < 5 && (nd << (p.lwpc + 1)) <= GATHER_SMEM_MAX && (p.nbits + p.lwpc) < 11) ++p.lwpc;
     p.lgH_in = lgH_in;
     p.lgH_out = lgH_out;
     fill_bits(grp, lgH_in, p.bits, p.nnb, p.nbit);
@@ -348,7 +375,7 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
     LCH_TRY(cu(launch_gather<R, POLY>(p, ngroups, s)));
     c->launches++;
     first = false;
-  } while (i < bits.size());
+  }
   if (first) {  // nothing to sum: T = T_in or 0
     if (t_in) return cu(cudaMemcpyAsync(t, t_in, bs_bytes(R, batch, lgH_out), cudaMemcpyDeviceToDevice, s));
     return cu(cudaMemsetAsync(t, 0, bs_bytes(R, batch, lgH_out), s));

@@ -702,6 +702,8 @@ constexpr int GNT = 512;  // gather threads per CTA
 
 // Tile bits are sorted, so the tile positions below 2^lgH_out (the outputs)
 // are exactly q < 2^nlow with nlow = #tile bits below lgH_out (base < 2^lgH_out).
+// A CTA covers one tile of 2^nbits positions for 2^lwpc consecutive lane-words
+// (small tiles take more words so every CTA moves >= ~64 KB).
 template <int R, uint32_t POLY>
 __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ GatherParams p) {
   constexpr int CH = R / 4;  // 16-byte chunks of one lane-word
@@ -712,8 +714,10 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
   int nlow = 0;
   while (nlow < p.nbits && p.bits[nlow] < p.lgH_out) ++nlow;
   const int nout = 1 << nlow;
-  uint4 *ytile = smem, *ttile = smem + np * CH;
-  const int w = blockIdx.y & 31, g = blockIdx.y >> 5;
+  const int lw = p.lwpc, WPC = 1 << lw;
+  const int wblocks = 32 >> lw;
+  const int g = blockIdx.y / wblocks, w0 = (blockIdx.y - g * wblocks) * WPC;
+  uint4 *ytile = smem, *ttile = smem + (np << lw) * CH;
   const uint32_t t = blockIdx.x;
   uint32_t base = 0;
   for (int i = 0; i < p.nnb; ++i) base |= ((t >> i) & 1u) << p.nbit[i];
@@ -724,25 +728,28 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
     for (int m = 0; m < p.nbits; ++m) o |= ((uint32_t(q) >> m) & 1u) << p.bits[m];
     return o;
   };
-  auto slot = [](int q, int c) { return q * CH + (c ^ ((q >> 1) & (CH - 1))); };
-  // stage lane-word w of every tile position (and of T_in at the outputs)
+  // e = q * WPC + word offset; the chunk swizzle keeps quarter-warps conflict-free
+  auto slot = [](int e, int c) { return e * CH + (c ^ ((e >> 1) & (CH - 1))); };
+  // stage lane-words [w0, w0 + WPC) of every tile position (and of T_in at the outputs)
   const uint4 *src = p.y + ((size_t(g) << p.lgH_in) * U4);
-  for (int idx = tid; idx < np * CH; idx += GNT) {
-    const int q = idx / CH, c = idx - q * CH;
-    cp_async16(ytile + slot(q, c), src + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w, c));
+  for (int idx = tid; idx < (np << lw) * CH; idx += GNT) {
+    const int e = idx / CH, c = idx - e * CH;
+    const int q = e >> lw, wl = e & (WPC - 1);
+    cp_async16(ytile + slot(e, c), src + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w0 + wl, c));
   }
   const uint4 *tin = p.t_in ? p.t_in + ((size_t(g) << p.lgH_out) * U4) : nullptr;
   if (tin)
-    for (int idx = tid; idx < nout * CH; idx += GNT) {
-      const int q = idx / CH, c = idx - q * CH;
-      cp_async16(ttile + slot(q, c), tin + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w, c));
+    for (int idx = tid; idx < (nout << lw) * CH; idx += GNT) {
+      const int e = idx / CH, c = idx - e * CH;
+      const int q = e >> lw, wl = e & (WPC - 1);
+      cp_async16(ttile + slot(e, c), tin + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w0 + wl, c));
     }
   cp_async_wait_all();
   __syncthreads();
-  auto ld = [&](const uint4 *tile, int q, uint32_t (&v)[R]) {
+  auto ld = [&](const uint4 *tile, int e, uint32_t (&v)[R]) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const uint4 x = tile[slot(q, c)];
+      const uint4 x = tile[slot(e, c)];
       v[4 * c + 0] = x.x;
       v[4 * c + 1] = x.y;
       v[4 * c + 2] = x.z;
@@ -750,10 +757,11 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
     }
   };
   uint4 *tout = p.t_out + ((size_t(g) << p.lgH_out) * U4);
-  for (int q = tid; q < nout; q += GNT) {
+  for (int e = tid; e < (nout << lw); e += GNT) {
+    const int q = e >> lw, wl = e & (WPC - 1);
     uint32_t acc[R];
     if (tin) {
-      ld(ttile, q, acc);
+      ld(ttile, e, acc);
     } else {
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] = 0u;
@@ -761,14 +769,14 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
     for (int m = 0; m < p.nbits; ++m) {
       if (m == p.sb || ((q >> m) & 1)) continue;
       uint32_t x[R];
-      ld(ytile, q | (1 << m), x);
+      ld(ytile, e | (1 << (m + lw)), x);
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= x[b];
     }
     if (p.sb >= 0) {  // q < nout has the special (top) bit clear
       uint32_t x[R], z[R], cz[R];
-      ld(ytile, q, x);
-      ld(ytile, q | (1 << p.sb), z);
+      ld(ytile, e, x);
+      ld(ytile, e | (1 << (p.sb + lw)), z);
 #pragma unroll
       for (int b = 0; b < R; ++b) z[b] ^= x[b];
       GF<R, POLY>::mul(cz, z, p.c);  // c is a kernel constant: uniform
@@ -778,7 +786,7 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
     const uint32_t pos = pos_of(q);
 #pragma unroll
     for (int c = 0; c < CH; ++c)
-      tout[size_t(pos) * U4 + Blk<R>::chunk(w, c)] =
+      tout[size_t(pos) * U4 + Blk<R>::chunk(w0 + wl, c)] =
           make_uint4(acc[4 * c + 0], acc[4 * c + 1], acc[4 * c + 2], acc[4 * c + 3]);
   }
 }
@@ -786,7 +794,7 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
 size_t gather_smem_bytes(int R, const GatherParams &p) {
   int nlow = 0;
   while (nlow < p.nbits && p.bits[nlow] < p.lgH_out) ++nlow;
-  return ((size_t(1) << p.nbits) + (p.t_in ? (size_t(1) << nlow) : 0)) * R * 4;
+  return (((size_t(1) << p.nbits) + (p.t_in ? (size_t(1) << nlow) : 0)) * R * 4) << p.lwpc;
 }
 
 // Walsh-Hadamard transform over Z_mod, bits [b0, b0 + tb) of each vector
@@ -968,7 +976,7 @@ cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(1u << (p.lgH_in - p.nbits), unsigned(ngroups) * 32u);
+  dim3 grid(1u << (p.lgH_in - p.nbits), unsigned(ngroups) * (32u >> p.lwpc));
   gather_kernel<R, POLY><<<grid, GNT, smem, s>>>(p);
   return cudaGetLastError();
 }

@@ -110,6 +110,7 @@ struct GatherParams {
   int lgH_in, lgH_out;
   int nnb;
   int nbit[16];
+  int lwpc;              // log2 lane-words per CTA (0..5)
   const uint4 *y;
   const uint4 *t_in;     // may be null
   uint4 *t_out;

@@ -145,6 +145,22 @@ int lch_decode_k(lch_ctx *ctx, const uint16_t *rx, int64_t stride_in,
                  int64_t batch, int64_t k, int64_t packet_len, const int64_t *host_counts,
                  void *stream);
 
+/* Host-buffer codec (the reference's host-array API, batch.py:110-153):
+ * inputs and outputs in host memory (page-locked for full overlap).  The
+ * batch streams through the GPU in chunks of `chunk` rows (codewords, or
+ * stripe groups when packet_len > 0; 0 = ~64 MiB per chunk): host->device
+ * copies, kernels and device->host copies of neighbouring chunks overlap on
+ * three streams.  Ordered on `stream` like the device entry points.  Layouts
+ * and semantics as lch_encode_k / lch_decode_k; erasure counts are taken
+ * from the host bitmasks (no device round trip). */
+int lch_encode_host(lch_ctx *ctx, const uint16_t *host_msg, int64_t stride_in,
+                    uint16_t *host_parity, int64_t stride_out, int64_t batch, int64_t k,
+                    int64_t packet_len, int64_t chunk, void *stream);
+int lch_decode_host(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride_in,
+                    const uint32_t *host_bits, int shared, uint16_t *host_out,
+                    int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len,
+                    int64_t chunk, void *stream);
+
 /* Device scratch budget per call (bytes, default 4 GiB): batches whose
  * bit-sliced intermediates exceed it are processed in lane chunks. */
 int lch_set_scratch_limit(lch_ctx *ctx, uint64_t bytes);

@@ -18,7 +18,7 @@ from . import _lib
 from ._lib import TooManyErasuresError
 from .basis import BasisTables
 from .derivative import run_derivative
-from .rs import CodeParams, decode_device, encode_device
+from .rs import CodeParams, decode_device, decode_host, encode_device, encode_host
 from .transform import run_transform
 
 
@@ -98,11 +98,23 @@ class BatchCodec:
     # -- public API ------------------------------------------------------------
 
     def encode(self, messages):
-        """Encode a (stripes x k) message matrix into (stripes x n) (batch.py:110-124)."""
+        """Encode a (stripes x k) message matrix into (stripes x n) (batch.py:110-124).
+
+        Host (numpy) matrices stream through the GPU in overlapped chunks
+        (lch_encode_host); CUDA tensors are encoded in place on the device."""
         cp = self.cp
         s, width = messages.shape
         if width != cp.k:
             raise ValueError(f"message width {width} != k={cp.k}")
+        if not _is_torch(messages):
+            _lib.require_cuda()
+            msg = np.ascontiguousarray(np.asarray(messages).astype(np.uint16, copy=False))
+            out = np.empty((s, cp.n), np.uint16)
+            out[:, :cp.k] = msg
+            if cp.n > cp.k and s > 0:
+                encode_host(cp, self.bt, msg, out[:, cp.k:])
+                _lib.torch_mod().cuda.current_stream().synchronize()
+            return out
         torch = _lib.torch_mod()
         md = self._dev(messages)
         out = torch.empty((s, cp.n), dtype=torch.int16, device="cuda")
@@ -149,11 +161,21 @@ class BatchCodec:
         for e in erased:
             if not 0 <= e < n:
                 raise ValueError(f"erasure position {e} outside field of size {n}")
+        if len(erased) > n - k:
+            raise TooManyErasuresError(f"{len(erased)} erasures exceed repair capacity {n - k}")
+        if not _is_torch(received):
+            rx = np.ascontiguousarray(np.asarray(received).astype(np.uint16, copy=False))
+            if not erased:
+                return rx[:, :k].copy()
+            _lib.require_cuda()
+            out = np.empty((rx.shape[0], k), np.uint16)
+            if rx.shape[0] > 0:
+                decode_host(cp, self.bt, rx, _lib.bitmask_from_positions(n, erased), out)
+                _lib.torch_mod().cuda.current_stream().synchronize()
+            return out
         rd = self._dev(received)
         if not erased:
             return self._back(received, rd[:, :k].contiguous())
-        if len(erased) > n - k:
-            raise TooManyErasuresError(f"{len(erased)} erasures exceed repair capacity {n - k}")
         torch = _lib.torch_mod()
         bits = _lib.to_device_u32(_lib.bitmask_from_positions(n, erased))
         out = torch.empty((rd.shape[0], k), dtype=torch.int16, device="cuda")

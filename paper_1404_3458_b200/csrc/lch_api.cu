@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <type_traits>
 #include <utility>
@@ -27,6 +28,7 @@ struct lch_ctx {
   int64_t launches = 0;
   size_t scratch_limit = size_t(4) << 30;
   std::vector<std::pair<int64_t, uint16_t *>> enc_tabs;  // encode-by-decode tables per k
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // host-buffer pipeline copy streams
   std::mutex mu;
 };
 
@@ -189,6 +191,19 @@ int build_rounds(const Plan &pl, PassParams &p) {
     for (int b = 0; b < tpb; ++b)
       if (b != cur.m0 && b != cur.m1) cur.obit[cur.nw++] = b;
     cur.op_end = p.nops;
+    // a pair's factor depends on the position bits above its level only
+    // (transform.py:123), so both pairs of an op share it when the round's
+    // other bit is a lower level
+    for (int o = cur.op_begin; o < cur.op_end; ++o) {
+      PassOp &op = p.ops[o];
+      const int other = op.m == 0 ? cur.m1 : cur.m0;
+      op.shared = (other >= 0 && pl.bits[other] < op.level) ? 1 : 0;
+    }
+    const int nr = cur.op_end - cur.op_begin;
+    cur.shape = 0;
+    if (cur.m1 >= 0 && nr == 1 && p.ops[cur.op_begin].m == 0) cur.shape = 1;
+    if (cur.m1 >= 0 && nr == 2 && p.ops[cur.op_begin].m == 0 && p.ops[cur.op_begin + 1].m == 1)
+      cur.shape = 2;
     p.rounds[p.nrounds++] = cur;
     cur = PassRound{};
     cur.m0 = cur.m1 = -1;
@@ -225,6 +240,7 @@ int build_rounds(const Plan &pl, PassParams &p) {
     o.level = op.level;
     o.hs = op.hs;
     o.table = nullptr;
+    o.shared = 0;
     o.m = (mb == cur.m0) ? 0 : 1;
     o.mloc = mb;
   }
@@ -265,9 +281,9 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     p.npre = int(pl.pre.size());
     p.npost = int(pl.post.size());
     for (int o = 0; o < p.npre; ++o)
-      p.pre[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.pre[o].table, pl.pre[o].tab_stride};
+      p.pre[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.pre[o].table, pl.pre[o].tab_stride, 0};
     for (int o = 0; o < p.npost; ++o)
-      p.post[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.post[o].table, pl.post[o].tab_stride};
+      p.post[o] = PassOp{OP_SCALE, 0, 0, 0, 0u, pl.post[o].table, pl.post[o].tab_stride, 0};
     p.tpb = int(pl.bits.size());
     p.lgH = lgH;
     fill_bits(pl.bits, lgH, p.gbit, p.nnb, p.nbit);
@@ -494,6 +510,8 @@ void lch_destroy(lch_ctx *c) {
     cudaFree(c->d_fwht_log);
     cudaFree(c->d_b_lo);
     for (auto &e : c->enc_tabs) cudaFree(e.second);
+    if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+    if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   }
   delete c;
 }
@@ -1050,6 +1068,187 @@ int lch_decode_k(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const uint32
                  const int64_t *host_counts, void *stream) {
   return decode_any(c, rx, stride_in, bits, shared, out, stride_out, batch, k, packet_len, host_counts,
                     stream);
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer pipeline: chunks of rows (codewords, or stripe groups in packet
+// layout) stream H2D on one stream, through the codec on the caller's
+// stream, and D2H on a third, NS slots deep, so the copies of chunk i +- 1
+// overlap the kernels of chunk i.  Everything is ordered after the work
+// already queued on `stream`, and `stream` waits for the last copy.
+
+}  // extern "C"
+
+namespace {
+
+struct HostArray {
+  const uint8_t *src = nullptr;  // host input (or null)
+  uint8_t *dst = nullptr;        // host output (or null)
+  size_t row_bytes = 0;          // bytes copied per row
+  size_t pitch = 0;              // host bytes between rows
+};
+
+int host_streams(lch_ctx *c) {
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->s_h2d) LCH_TRY(cu(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking)));
+  if (!c->s_d2h) LCH_TRY(cu(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking)));
+  return LCH_OK;
+}
+
+// ins: host inputs copied per chunk; out: the host output; compute(d_ins,
+// d_out, row0, rows) runs the codec on the caller's stream.
+using ChunkFn = std::function<int(const std::vector<const uint8_t *> &, uint8_t *, int64_t, int64_t)>;
+
+int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
+                  const std::vector<HostArray> &ins, const HostArray &out, const ChunkFn &compute) {
+  constexpr int NS = 3;
+  LCH_TRY(host_streams(c));
+  const int ni = int(ins.size());
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&](cudaEvent_t &e) -> int {
+    LCH_TRY(cu(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)));
+    evs.push_back(e);
+    return LCH_OK;
+  };
+  struct Guard {
+    std::vector<cudaEvent_t> *v;
+    ~Guard() {
+      for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    }
+  } guard{&evs};
+  Scratch sc(s);
+  std::vector<uint8_t *> din(size_t(NS) * ni, nullptr), dout(NS, nullptr);
+  for (int k = 0; k < NS; ++k) {
+    for (int a = 0; a < ni; ++a) LCH_TRY(sc.alloc(din[size_t(k) * ni + a], ins[a].row_bytes * size_t(chunk)));
+    LCH_TRY(sc.alloc(dout[k], out.row_bytes * size_t(chunk)));
+  }
+  cudaEvent_t entry, ev_in[NS], ev_done[NS], ev_free[NS];
+  LCH_TRY(mkev(entry));
+  for (int k = 0; k < NS; ++k) {
+    LCH_TRY(mkev(ev_in[k]));
+    LCH_TRY(mkev(ev_done[k]));
+    LCH_TRY(mkev(ev_free[k]));
+  }
+  LCH_TRY(cu(cudaEventRecord(entry, s)));
+  LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, entry, 0)));
+  LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, entry, 0)));
+  const int64_t nchunks = (rows + chunk - 1) / chunk;
+  for (int64_t i = 0; i < nchunks; ++i) {
+    const int k = int(i % NS);
+    const int64_t r0 = i * chunk, nr = std::min(chunk, rows - r0);
+    if (i >= NS) LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, ev_free[k], 0)));
+    std::vector<const uint8_t *> dptr(static_cast<size_t>(ni), nullptr);
+    for (int a = 0; a < ni; ++a) {
+      const HostArray &h = ins[a];
+      uint8_t *d = din[size_t(k) * ni + a];
+      LCH_TRY(cu(cudaMemcpy2DAsync(d, h.row_bytes, h.src + size_t(r0) * h.pitch, h.pitch, h.row_bytes,
+                                   size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
+      dptr[size_t(a)] = d;
+    }
+    LCH_TRY(cu(cudaEventRecord(ev_in[k], c->s_h2d)));
+    LCH_TRY(cu(cudaStreamWaitEvent(s, ev_in[k], 0)));
+    const int crc = compute(dptr, dout[k], r0, nr);
+    if (crc != LCH_OK) return crc;
+    LCH_TRY(cu(cudaEventRecord(ev_done[k], s)));
+    LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, ev_done[k], 0)));
+    LCH_TRY(cu(cudaMemcpy2DAsync(out.dst + size_t(r0) * out.pitch, out.pitch, dout[k], out.row_bytes,
+                                 out.row_bytes, size_t(nr), cudaMemcpyDeviceToHost, c->s_d2h)));
+    LCH_TRY(cu(cudaEventRecord(ev_free[k], c->s_d2h)));
+  }
+  for (int64_t i = std::max<int64_t>(0, nchunks - NS); i < nchunks; ++i)
+    LCH_TRY(cu(cudaStreamWaitEvent(s, ev_free[i % NS], 0)));
+  return LCH_OK;
+}
+
+int64_t popcount_words(const uint32_t *w, int64_t n) {
+  int64_t c = 0;
+  for (int64_t i = 0; i < n; ++i) c += __builtin_popcount(w[i]);
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lch_encode_host(lch_ctx *c, const uint16_t *host_msg, int64_t stride_in, uint16_t *host_parity,
+                    int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len, int64_t chunk,
+                    void *stream) {
+  if (!c || !host_msg || batch < 0 || chunk < 0 || packet_len < 0) return LCH_EINVAL;
+  const int64_t n = int64_t(c->t.order), pkt = packet_len;
+  if (k < 1 || k > n || stride_in < k || (k < n && (!host_parity || stride_out < n - k))) return LCH_EINVAL;
+  if (pkt && (pkt % GROUP || batch % pkt)) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0 || k == n) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // rows: codewords, or stripe groups of pkt lanes
+  const int64_t rows = pkt ? batch / pkt : batch, lanes_per_row = pkt ? pkt : 1;
+  const size_t in_row = size_t(k * lanes_per_row) * 2, out_row = size_t((n - k) * lanes_per_row) * 2;
+  if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / std::max(in_row, out_row)));
+  chunk = std::min(chunk, rows);
+  std::vector<HostArray> ins(1);
+  ins[0].src = reinterpret_cast<const uint8_t *>(host_msg);
+  ins[0].row_bytes = in_row;
+  ins[0].pitch = size_t(stride_in * lanes_per_row) * 2;
+  HostArray out;
+  out.dst = reinterpret_cast<uint8_t *>(host_parity);
+  out.row_bytes = out_row;
+  out.pitch = size_t(stride_out * lanes_per_row) * 2;
+  return host_pipeline(c, s, rows, chunk, ins, out,
+                       [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr) {
+                         return encode_any(c, reinterpret_cast<const uint16_t *>(d[0]), k,
+                                           reinterpret_cast<uint16_t *>(o), n - k, nr * lanes_per_row, k,
+                                           pkt, stream);
+                       });
+}
+
+int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, const uint32_t *host_bits,
+                    int shared, uint16_t *host_out, int64_t stride_out, int64_t batch, int64_t k,
+                    int64_t packet_len, int64_t chunk, void *stream) {
+  if (!c || !host_rx || !host_bits || !host_out || batch < 0 || chunk < 0 || packet_len < 0)
+    return LCH_EINVAL;
+  const int64_t n = int64_t(c->t.order), pkt = packet_len;
+  if (k < 1 || k > n || stride_in < n || stride_out < k) return LCH_EINVAL;
+  if (pkt && (pkt % GROUP || batch % pkt)) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0) return LCH_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t words = std::max<int64_t>(n / 32, 1);
+  const int64_t rows = pkt ? batch / pkt : batch, lanes_per_row = pkt ? pkt : 1;
+  // erasure counts from the host bitmasks (no device round trip)
+  const int64_t npat = shared ? 1 : rows;
+  std::vector<int64_t> counts(static_cast<size_t>(npat), 0);
+  for (int64_t i = 0; i < npat; ++i) {
+    counts[size_t(i)] = popcount_words(host_bits + i * words, words);
+    if (counts[size_t(i)] > n - k) return LCH_ETOOMANY;  // rs.py:121-123
+  }
+  Scratch sc(s);
+  uint32_t *d_shared = nullptr;
+  if (shared) {
+    LCH_TRY(sc.alloc(d_shared, size_t(words)));
+    LCH_TRY(cu(cudaMemcpyAsync(d_shared, host_bits, size_t(words) * 4, cudaMemcpyHostToDevice, s)));
+  }
+  const size_t in_row = size_t(n * lanes_per_row) * 2, out_row = size_t(k * lanes_per_row) * 2;
+  if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / in_row));
+  chunk = std::min(chunk, rows);
+  std::vector<HostArray> ins(shared ? 1 : 2);
+  ins[0].src = reinterpret_cast<const uint8_t *>(host_rx);
+  ins[0].row_bytes = in_row;
+  ins[0].pitch = size_t(stride_in * lanes_per_row) * 2;
+  if (!shared) {
+    ins[1].src = reinterpret_cast<const uint8_t *>(host_bits);
+    ins[1].row_bytes = ins[1].pitch = size_t(words) * 4;
+  }
+  HostArray out;
+  out.dst = reinterpret_cast<uint8_t *>(host_out);
+  out.row_bytes = out_row;
+  out.pitch = size_t(stride_out * lanes_per_row) * 2;
+  return host_pipeline(c, s, rows, chunk, ins, out,
+                       [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr) {
+                         const uint32_t *bits = shared ? d_shared : reinterpret_cast<const uint32_t *>(d[1]);
+                         return decode_any(c, reinterpret_cast<const uint16_t *>(d[0]), n, bits, shared,
+                                           reinterpret_cast<uint16_t *>(o), k, nr * lanes_per_row, k, pkt,
+                                           counts.data() + (shared ? 0 : r0), stream);
+                       });
 }
 
 int lch_set_scratch_limit(lch_ctx *c, uint64_t bytes) {

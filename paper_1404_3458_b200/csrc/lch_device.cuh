@@ -6,8 +6,8 @@
 // (field.py:1-13: element index == representation); multiplication by a
 // warp-uniform constant f is evaluated by a Horner scheme over the 2-bit
 // digits of f, using only XORs of whole planes:
-//     f*v = (((d_top * v) x^2 + d_.. * v) x^2 + ...) ,  d * v in {0, v, xv, v+xv}
-// where x*v is a plane rotation plus XORs at the taps of the reduction
+//     f*v = sum_t d_t * (x^(2t) v),  d * p in {0, p, xp, p+xp}
+// where x*p is a plane rotation plus XORs at the taps of the reduction
 // polynomial.  All 32 symbols of a word share the factor, so one thread
 // multiplies 32 symbols with ~R/2 * (R + taps) XORs.
 #pragma once
@@ -68,99 +68,122 @@ struct GF {
     return d == 0 ? 0u : d == 1 ? (1u << b) : d == 2 ? s1(b) : (s1(b) ^ (1u << b));
   }
 
-  // acc <- (SQ ? x^2 * acc : 0) + D * v.  Every output plane is the XOR of at
-  // most 5 planes (<= 2 LOP3s); the digit term's planes come first so each
-  // LOP3 is unique to its digit branch and the compiler cannot hoist the
-  // reduction taps out of the branches (which would cost an extra XOR).
-  template <bool SQ, int D>
-  __device__ __forceinline__ static void step(uint32_t (&acc)[R], const uint32_t (&v)[R]) {
-    uint32_t o[R];
+  // x ^ XOR_{s in m} p[s] (m a compile-time plane set once the callers'
+  // plane loops are unrolled): terms paired into 3-input LOP3s.
+  __device__ __forceinline__ static uint32_t xor_into_set(uint32_t x, const uint32_t (&p)[R],
+                                                          uint32_t m) {
+    uint32_t pend = 0u;
+    bool has = false;
 #pragma unroll
-    for (int b = 0; b < R; ++b) {
-      const uint32_t am = SQ ? s2(b) : 0u, vm = dmask(D, b);
-      uint32_t t[6];
-      int n = 0;
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if ((vm >> i) & 1u) t[n++] = v[i];
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-        if ((am >> i) & 1u) t[n++] = acc[i];
-      uint32_t x = n ? t[0] : 0u;
-      int i = 1;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        if (n - i >= 2) {
-          x = lop3_xor(x, t[i], t[i + 1]);
-          i += 2;
-        } else if (n - i == 1) {
-          x ^= t[i];
-          i += 1;
+    for (int s = 0; s < R; ++s) {
+      if ((m >> s) & 1u) {
+        if (has) {
+          x = lop3_xor(x, pend, p[s]);
+          has = false;
+        } else {
+          pend = p[s];
+          has = true;
         }
       }
-      o[b] = x;
+    }
+    return has ? (x ^ pend) : x;
+  }
+  // XOR_{s in m} p[s]
+  __device__ __forceinline__ static uint32_t xor_set(const uint32_t (&p)[R], uint32_t m) {
+    if (m == 0u) return 0u;
+    const int s0 = lowbit(m);
+    return xor_into_set(p[s0], p, m & (m - 1u));
+  }
+
+  // u += f * v for a warp-uniform f.  f v = sum_t d_t (x^(2t) v) over the
+  // 2-bit digits d_t of f, least significant first: p = x^(2t) v advances
+  // unconditionally (plane renames plus the reduction taps) and only
+  // u += d_t p (d p in {p, x p, (1 + x) p}) sits under the warp-uniform digit
+  // branch, updating u in place, so the branch paths join without register
+  // moves.  ~R/2 * (R + taps) XORs per 32 symbols.
+  __device__ __forceinline__ static void mul_acc(uint32_t (&u)[R], const uint32_t (&v)[R],
+                                                 uint32_t f) {
+    uint32_t p[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) p[b] = v[b];
+#pragma unroll
+    for (int t = 0; t < ND; ++t) {
+      const uint32_t d = (f >> (2 * t)) & 3u;
+      if (d == 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] ^= p[b];
+      } else if (d == 2u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] = xor_into_set(u[b], p, dmask(2, b));
+      } else if (d == 3u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] = xor_into_set(u[b], p, dmask(3, b));
+      }
+      if (t + 1 < ND) {
+        uint32_t q[R];
+#pragma unroll
+        for (int b = 0; b < R; ++b) q[b] = xor_set(p, s2(b));
+#pragma unroll
+        for (int b = 0; b < R; ++b) p[b] = q[b];
+      }
+    }
+  }
+
+  // u0 += f * v0 and u1 += f * v1 under one digit dispatch (twice the
+  // independent work per warp-uniform branch).
+  __device__ __forceinline__ static void mul_acc2(uint32_t (&u0)[R], const uint32_t (&v0)[R],
+                                                  uint32_t (&u1)[R], const uint32_t (&v1)[R],
+                                                  uint32_t f) {
+    uint32_t p0[R], p1[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      p0[b] = v0[b];
+      p1[b] = v1[b];
     }
 #pragma unroll
-    for (int b = 0; b < R; ++b) acc[b] = o[b];
-  }
-
-  template <bool SQ>
-  __device__ __forceinline__ static void digit(uint32_t (&acc)[R], const uint32_t (&v)[R],
-                                               uint32_t f, int t) {
-    const uint32_t hi = f & (2u << (2 * t)), lo = f & (1u << (2 * t));
-    if (hi) {
-      if (lo)
-        step<SQ, 3>(acc, v);
-      else
-        step<SQ, 2>(acc, v);
-    } else {
-      if (lo)
-        step<SQ, 1>(acc, v);
-      else
-        step<SQ, 0>(acc, v);
+    for (int t = 0; t < ND; ++t) {
+      const uint32_t d = (f >> (2 * t)) & 3u;
+      if (d == 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] ^= p0[b];
+          u1[b] ^= p1[b];
+        }
+      } else if (d == 2u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] = xor_into_set(u0[b], p0, dmask(2, b));
+          u1[b] = xor_into_set(u1[b], p1, dmask(2, b));
+        }
+      } else if (d == 3u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] = xor_into_set(u0[b], p0, dmask(3, b));
+          u1[b] = xor_into_set(u1[b], p1, dmask(3, b));
+        }
+      }
+      if (t + 1 < ND) {
+        uint32_t q0[R], q1[R];
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          q0[b] = xor_set(p0, s2(b));
+          q1[b] = xor_set(p1, s2(b));
+        }
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          p0[b] = q0[b];
+          p1[b] = q1[b];
+        }
+      }
     }
   }
 
-  // acc = f * v for a warp-uniform f: Horner over the 2-bit digits of f,
-  // d * v in {0, v, x v, (1 + x) v}; digits tested bit by bit.
+  // acc = f * v
   __device__ __forceinline__ static void mul(uint32_t (&acc)[R], const uint32_t (&v)[R],
                                              uint32_t f) {
-    digit<false>(acc, v, f, ND - 1);
 #pragma unroll
-    for (int t = ND - 2; t >= 0; --t) digit<true>(acc, v, f, t);
-  }
-
-  // Two independent vectors sharing one warp-uniform factor: one digit
-  // dispatch per step drives both (twice the independent work per branch).
-  template <bool SQ>
-  __device__ __forceinline__ static void digit2(uint32_t (&a0)[R], uint32_t (&a1)[R],
-                                                const uint32_t (&v0)[R], const uint32_t (&v1)[R],
-                                                uint32_t f, int t) {
-    const uint32_t hi = f & (2u << (2 * t)), lo = f & (1u << (2 * t));
-    if (hi) {
-      if (lo) {
-        step<SQ, 3>(a0, v0);
-        step<SQ, 3>(a1, v1);
-      } else {
-        step<SQ, 2>(a0, v0);
-        step<SQ, 2>(a1, v1);
-      }
-    } else {
-      if (lo) {
-        step<SQ, 1>(a0, v0);
-        step<SQ, 1>(a1, v1);
-      } else {
-        step<SQ, 0>(a0, v0);
-        step<SQ, 0>(a1, v1);
-      }
-    }
-  }
-  __device__ __forceinline__ static void mul2(uint32_t (&a0)[R], uint32_t (&a1)[R],
-                                              const uint32_t (&v0)[R], const uint32_t (&v1)[R],
-                                              uint32_t f) {
-    digit2<false>(a0, a1, v0, v1, f, ND - 1);
-#pragma unroll
-    for (int t = ND - 2; t >= 0; --t) digit2<true>(a0, a1, v0, v1, f, t);
+    for (int b = 0; b < R; ++b) acc[b] = 0u;
+    mul_acc(acc, v, f);
   }
 
   // acc = f_lane * v where the factor differs per lane (not warp-uniform):

@@ -426,12 +426,24 @@ template <int R, uint32_t POLY>
 __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv) {
   using F = GF<R, POLY>;
   if (inv) F::xor_into(v, u);
-  if (f) {
-    uint32_t t[R];
-    F::mul(t, v, f);
-    F::xor_into(u, t);
-  }
+  F::mul_acc(u, v, f);
   if (!inv) F::xor_into(v, u);
+}
+
+// Two butterflies sharing one factor (pairs (u0, v0) and (u1, v1)).
+template <int R, uint32_t POLY>
+__device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R], uint32_t (&u1)[R],
+                                           uint32_t (&v1)[R], uint32_t f, bool inv) {
+  using F = GF<R, POLY>;
+  if (inv) {
+    F::xor_into(v0, u0);
+    F::xor_into(v1, u1);
+  }
+  F::mul_acc2(u0, v0, u1, v1, f);
+  if (!inv) {
+    F::xor_into(v0, u0);
+    F::xor_into(v1, u1);
+  }
 }
 
 // Butterfly factors of one tile (transform.py:112,123: w_hat[i][c >> (i+1)] ^
@@ -542,7 +554,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       int q0 = 0;
       for (int j = 0; j < rr.nw; ++j) q0 |= ((warp >> j) & 1) << rr.obit[j];
       uint32_t a0[R], a1[R], a2[R], a3[R];
-      if (active) {
+      if (active && !(p.dbg & 32)) {
         Blk<R>::load(bsm + q0 * U4, lane, a0);
         Blk<R>::load(bsm + (q0 | M0) * U4, lane, a1);
         if (has1) {
@@ -556,10 +568,41 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         if (has_next) {
           const uint32_t nb = base_of(next);
           issue_tile<R>(p, smem, tpos, next / ntile, nb, TP, &bar);
-          nfl.fetch(p, tpos, nb);
+          if (!(p.dbg & 64)) nfl.fetch(p, tpos, nb);
         }
       }
-      if (active) {
+      if (active && rr.shape != 0 && !(p.dbg & 2)) {
+        // straight-line rounds: [op along m0] or [op along m0, op along m1];
+        // ops whose pairs share the factor run as one two-vector multiply
+        const uint32_t *ft = fac[fb] + rr.op_begin * (1 << TPB_MAX);
+        const PassOp &oa = p.ops[rr.op_begin];
+        const uint32_t fa = __shfl_sync(0xffffffffu, ft[q0], 0);
+        if (oa.shared) {
+          butterfly2<R, POLY>(a0, a1, a2, a3, fa, oa.kind == OP_INV);
+        } else {
+          const uint32_t fa2 = __shfl_sync(0xffffffffu, ft[q0 | M1], 0);
+          butterfly<R, POLY>(a0, a1, fa, oa.kind == OP_INV);
+          butterfly<R, POLY>(a2, a3, fa2, oa.kind == OP_INV);
+        }
+        if (rr.shape == 2) {
+          const uint32_t *fu = ft + (1 << TPB_MAX);
+          const PassOp &ob = p.ops[rr.op_begin + 1];
+          const uint32_t fb1 = __shfl_sync(0xffffffffu, fu[q0], 0);
+          if (ob.shared) {
+            butterfly2<R, POLY>(a0, a2, a1, a3, fb1, ob.kind == OP_INV);
+          } else {
+            const uint32_t fb2 = __shfl_sync(0xffffffffu, fu[q0 | M0], 0);
+            butterfly<R, POLY>(a0, a2, fb1, ob.kind == OP_INV);
+            butterfly<R, POLY>(a1, a3, fb2, ob.kind == OP_INV);
+          }
+        }
+        if (!last_reg && !(p.dbg & 32)) {
+          Blk<R>::store(bsm + q0 * U4, lane, a0);
+          Blk<R>::store(bsm + (q0 | M0) * U4, lane, a1);
+          Blk<R>::store(bsm + (q0 | M1) * U4, lane, a2);
+          Blk<R>::store(bsm + (q0 | M0 | M1) * U4, lane, a3);
+        }
+      } else if (active) {
         // A round's ops are [along m0]* [along m1]*.  Along m0 the pairs are
         // (a0,a1), (a2,a3); at the first m1 op a1 and a2 swap once, so the same
         // two inlined butterflies (one multiply body each) serve both bits.
@@ -612,7 +655,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
             Blk<R>::store(dst + size_t(base | tpos[q0 | M0 | M1]) * U4, lane, a3);
           }
         }
-        if (has_next) nfl.put(fac[fb ^ 1]);
+        if (has_next && !(p.dbg & 64)) nfl.put(fac[fb ^ 1]);
       } else if (last_reg) {
         // Drain the tile through the staging half-buffer with bulk stores
         // (asynchronous: they overlap the next tile's rounds).
@@ -640,7 +683,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
             tma_store_commit();
           }
         }
-        if (has_next) nfl.put(fac[fb ^ 1]);
+        if (has_next && !(p.dbg & 64)) nfl.put(fac[fb ^ 1]);
       }
       if (!last_reg) __syncthreads();
     }
@@ -678,8 +721,10 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         const uint32_t nb = base_of(next);
         issue_tile<R>(p, smem, tpos, next / ntile, nb, TP, &bar);
         FactorLoader fl;
-        fl.fetch(p, tpos, nb);
-        fl.put(fac[fb ^ 1]);
+        if (!(p.dbg & 64)) {
+          fl.fetch(p, tpos, nb);
+          fl.put(fac[fb ^ 1]);
+        }
       }
     }
     if (!has_next) {

@@ -26,6 +26,8 @@ struct PassOp {
   uint32_t hs;            // W^_i(shift) (0 for shift 0)
   const uint16_t *table;  // per-position factors (SCALE), indexed by position
   int64_t tab_stride;     // SCALE: + (stripe group) * tab_stride (0: one row for all)
+  int shared;             // FWD/INV: both pairs of the round share the factor (the
+                          // other round bit lies below the level, transform.py:123)
 };
 
 // A round: every thread holds the 4 positions spanned by tile bits m0, m1
@@ -36,6 +38,7 @@ struct PassRound {
   int nw;
   int obit[TPB_MAX];
   int op_begin, op_end;   // butterfly ops of the round in ops[]
+  int shape;              // 0 general; 1: one op along m0; 2: one along m0 then one along m1
 };
 
 // Raw uint16 batch: element (b, j) at ptr[b * row_stride + j].

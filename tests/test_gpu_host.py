@@ -1,0 +1,140 @@
+"""Host-buffer pipeline (lch_encode_host / lch_decode_host): chunked H2D /
+kernel / D2H overlap must give exactly the device-path results, which are
+themselves pinned to the oracle (test_gpu_parity.py, test_gpu_stripe.py)."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lch():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1404_3458_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def bt8(lch):
+    return lch.build_basis_tables(lch.tables_for(8), 256)
+
+
+@pytest.fixture(scope="module")
+def bt16(lch):
+    return lch.build_basis_tables(lch.tables_for(16), 1 << 16)
+
+
+def pinned(a):
+    import torch
+    t = torch.empty(a.shape, dtype=torch.int16, pin_memory=True)
+    t.numpy().view(np.uint16)[...] = a
+    return t
+
+
+@pytest.mark.parametrize("chunk", [0, 1, 7, 700])
+def test_encode_decode_host_r8(lch, bt8, orc8, chunk):
+    import torch
+    from paper_1404_3458_b200.rs import decode_host, encode_host
+    cp = lch.CodeParams(8, 128)
+    B = 1500
+    msg = O.gen_symbols(11, 8, 0, B, 128)
+    hm = pinned(msg)
+    hp = torch.empty((B, 128), dtype=torch.int16, pin_memory=True)
+    encode_host(cp, bt8, hm, hp, chunk)
+    torch.cuda.synchronize()
+    par = hp.numpy().view(np.uint16)
+    np.testing.assert_array_equal(par, orc8.encode_batch(128, msg, nthreads=8))
+    cw = np.concatenate([msg, par], axis=1)
+    # shared pattern
+    mask = O.gen_erasures(12, 256, 128, 0, 1)[0].astype(bool)
+    rx = cw.copy()
+    rx[:, mask] = 0x55
+    out = torch.empty((B, 128), dtype=torch.int16, pin_memory=True)
+    from paper_1404_3458_b200._lib import bitmask_from_positions
+    hrx = pinned(rx)
+    decode_host(cp, bt8, hrx, bitmask_from_positions(256, np.nonzero(mask)[0]), out, chunk)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.numpy().view(np.uint16), msg)
+    # per-codeword patterns
+    masks = O.gen_erasures(13, 256, 128, 0, B).astype(bool)
+    rx = np.where(masks, 0x77, cw).astype(np.uint16)
+    bits = np.stack([bitmask_from_positions(256, np.nonzero(m)[0]) for m in masks])
+    out2 = torch.empty((B, 128), dtype=torch.int16, pin_memory=True)
+    hrx2 = pinned(rx)
+    decode_host(cp, bt8, hrx2, bits, out2, chunk)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out2.numpy().view(np.uint16), msg)
+
+
+def test_batchcodec_numpy_paths(lch, bt8, orc8):
+    cp = lch.CodeParams(8, 64)
+    codec = lch.BatchCodec(cp, bt8)
+    msg = O.gen_symbols(21, 8, 0, 300, 64)
+    cw = codec.encode(msg)
+    assert isinstance(cw, np.ndarray) and cw.shape == (300, 256)
+    np.testing.assert_array_equal(cw[:, :64], msg)
+    np.testing.assert_array_equal(cw[:, 64:], orc8.encode_batch(64, msg, nthreads=8))
+    erased = set(range(0, 256, 2)) | {1, 3, 5}
+    rx = cw.copy()
+    rx[:, sorted(erased)] = 0
+    np.testing.assert_array_equal(codec.decode(rx, erased), msg)
+    with pytest.raises(lch.TooManyErasuresError):
+        codec.decode(rx, set(range(193)))
+
+
+def test_host_r16_matches_device(lch, bt16):
+    import torch
+    from paper_1404_3458_b200 import gen
+    from paper_1404_3458_b200.rs import decode_device, decode_host, encode_device, encode_host
+    cp = lch.CodeParams(16, 1 << 15)
+    B, K, N = 600, 1 << 15, 1 << 16
+    dmsg = gen.symbols(bt16.ctx, 5, 0, B, K)
+    dpar = torch.empty((B, K), dtype=torch.int16, device="cuda")
+    encode_device(cp, bt16, dmsg, dpar)
+    hm = dmsg.cpu().pin_memory()
+    hp = torch.empty((B, K), dtype=torch.int16, pin_memory=True)
+    encode_host(cp, bt16, hm, hp, 128)
+    torch.cuda.synchronize()
+    assert torch.equal(hp, dpar.cpu())
+    mask = gen.erasure_masks(bt16.ctx, 6, N, N - K, 0, 1)
+    bits_d = gen.mask_to_bits(mask)[0].contiguous()
+    rx = torch.cat([dmsg, dpar], dim=1)
+    rx[:, mask[0]] = 0
+    hout = torch.empty((B, K), dtype=torch.int16, pin_memory=True)
+    hrx = rx.cpu().pin_memory()  # kept alive until the stream is synchronised
+    decode_host(cp, bt16, hrx, bits_d.cpu().numpy().view(np.uint32), hout, 200)
+    torch.cuda.synchronize()
+    assert torch.equal(hout, dmsg.cpu())
+
+
+def test_packet_host_pipeline(lch, bt8):
+    """Packet layout through the host pipeline (rows = stripe groups)."""
+    import torch
+    from paper_1404_3458_b200 import _lib, gen
+    P, G, k, n = 1024, 5, 192, 256
+    sc = lch.StripeCodec(bt8, k, P)
+    msg = gen.packets(bt8.ctx, 31, 0, G, k, P)
+    par = sc.encode(msg)
+    hm = msg.cpu().pin_memory()
+    hp = torch.empty((G, n - k, P), dtype=torch.int16, pin_memory=True)
+    _lib.check(_lib.lib.lch_encode_host(bt8.ctx.handle, hm.data_ptr(), k, hp.data_ptr(), n - k, G * P, k,
+                                        P, 2, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(hp, par.cpu())
+    masks = O.gen_erasures(32, n, n - k, 0, G).astype(bool)
+    from paper_1404_3458_b200._lib import bitmask_from_positions
+    bits = np.stack([bitmask_from_positions(n, np.nonzero(m)[0]) for m in masks])
+    rx = torch.cat([hm, hp], dim=1)
+    for g in range(G):
+        rx[g, torch.from_numpy(masks[g])] = 0
+    hout = torch.empty((G, k, P), dtype=torch.int16, pin_memory=True)
+    hrx = rx.pin_memory()
+    _lib.check(_lib.lib.lch_decode_host(bt8.ctx.handle, hrx.data_ptr(), n, bits.ctypes.data, 0,
+                                        hout.data_ptr(), k, G * P, k, P, 2, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(hout, hm)

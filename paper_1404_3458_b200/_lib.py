@@ -16,7 +16,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "_build", "liblch.so")
+SO_PATH = os.environ.get("LCH_SO_PATH") or os.path.join(_HERE, "_build", "liblch.so")
 
 LCH_OK = 0
 LCH_EINVAL = -1

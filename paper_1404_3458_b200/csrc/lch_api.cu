@@ -424,6 +424,32 @@ int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out
                  cudaStream_t s, const DecodeEpi *epi = nullptr) {
   const int r = c->t.r;
   const size_t n = size_t(1) << r;
+  const bool aligned = !epi || (reinterpret_cast<uintptr_t>(epi->rx) % 16 == 0 &&
+                                reinterpret_cast<uintptr_t>(epi->phi) % 16 == 0 && epi->rx_stride % 8 == 0);
+  if (r == 16 && aligned) {
+    FwhtParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.nvec = np;
+    p.lgn = r;
+    p.mod = c->t.m;
+    p.bits = bits;
+    p.post_mul = c->d_fwht_log;
+    p.exp = c->d_exp;
+    p.loc_out = loc_out;
+    p.log_out = log_out;
+    if (epi) {
+      p.bits_e = bits;
+      p.rx = epi->rx;
+      p.rx_stride = epi->rx_stride;
+      p.log = c->d_log;
+      p.phi = epi->phi;
+      p.pinv_log = epi->pinv_log;
+      p.k = epi->k;
+    }
+    LCH_TRY(cu(launch_locator16(p, s)));
+    c->launches++;
+    return LCH_OK;
+  }
   Scratch sc(s);
   uint32_t *buf = nullptr;
   LCH_TRY(sc.alloc(buf, size_t(np) * n));

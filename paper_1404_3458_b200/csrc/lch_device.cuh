@@ -129,6 +129,64 @@ struct GF {
     }
   }
 
+#ifndef LCH_MUL_2BIT
+  // 1-bit digits: one warp-uniform branch per bit of f (fewer taken
+  // branches than the 2-bit digits below: measured 4-5% faster passes)
+  __device__ __forceinline__ static void mul_acc_1(uint32_t (&u)[R], const uint32_t (&v)[R],
+                                                   uint32_t f) {
+    uint32_t p[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) p[b] = v[b];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      if ((f >> t) & 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] ^= p[b];
+      }
+      if (t + 1 < R) {
+        uint32_t q[R];
+#pragma unroll
+        for (int b = 0; b < R; ++b) q[b] = xor_set(p, s1(b));
+#pragma unroll
+        for (int b = 0; b < R; ++b) p[b] = q[b];
+      }
+    }
+  }
+  __device__ __forceinline__ static void mul_acc2_1(uint32_t (&u0)[R], const uint32_t (&v0)[R],
+                                                    uint32_t (&u1)[R], const uint32_t (&v1)[R],
+                                                    uint32_t f) {
+    uint32_t p0[R], p1[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      p0[b] = v0[b];
+      p1[b] = v1[b];
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      if ((f >> t) & 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] ^= p0[b];
+          u1[b] ^= p1[b];
+        }
+      }
+      if (t + 1 < R) {
+        uint32_t q0[R], q1[R];
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          q0[b] = xor_set(p0, s1(b));
+          q1[b] = xor_set(p1, s1(b));
+        }
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          p0[b] = q0[b];
+          p1[b] = q1[b];
+        }
+      }
+    }
+  }
+#endif
+
   // u0 += f * v0 and u1 += f * v1 under one digit dispatch (twice the
   // independent work per warp-uniform branch).
   __device__ __forceinline__ static void mul_acc2(uint32_t (&u0)[R], const uint32_t (&v0)[R],

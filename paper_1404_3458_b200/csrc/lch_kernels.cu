@@ -426,7 +426,11 @@ template <int R, uint32_t POLY>
 __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv) {
   using F = GF<R, POLY>;
   if (inv) F::xor_into(v, u);
+#ifndef LCH_MUL_2BIT
+  F::mul_acc_1(u, v, f);
+#else
   F::mul_acc(u, v, f);
+#endif
   if (!inv) F::xor_into(v, u);
 }
 
@@ -439,7 +443,11 @@ __device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R],
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);
   }
+#ifndef LCH_MUL_2BIT
+  F::mul_acc2_1(u0, v0, u1, v1, f);
+#else
   F::mul_acc2(u0, v0, u1, v1, f);
+#endif
   if (!inv) {
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);
@@ -893,6 +901,146 @@ __global__ void fwht_kernel(const __grid_constant__ FwhtParams p) {
   } else {
     p.data[idx] = x;
   }
+}
+
+// Whole erasure locator of one pattern per CTA for r = 16 (walsh.py:97-114):
+// R^w = FWHT(FWHT(indicator) * FWHT(log)) mod 2^16 - 1, the 2^16 residues
+// held in shared memory as uint16 (ones' complement: 0xFFFF == 0 until the
+// final normalisation).  The Walsh-Hadamard stages commute, so the two
+// transforms run as rounds over 4-bit groups G0, G1, G2, G3 | G3, G2, G1, G0
+// with the pointwise product fused into the G3 round (7 shared-memory round
+// trips, 16 values per thread slot in registers).  The first round reads the
+// indicator straight from the bitmask; the last writes the epilogue (locator
+// values / logs, or phi = rx * Pi_bar and -log Pi' for the decode).
+constexpr int LOC_NT = 1024;
+
+__device__ __forceinline__ uint32_t fold16(uint32_t x) { return (x & 0xFFFFu) + (x >> 16); }
+
+__device__ __forceinline__ void wht16(uint32_t (&v)[16]) {
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1)
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (!(e & h)) {
+        const uint32_t a = v[e], b = v[e | h];
+        v[e] = fold16(a + b);
+        v[e | h] = fold16(a + (b ^ 0xFFFFu));  // a - b mod 2^16 - 1
+      }
+}
+
+__global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant__ FwhtParams p) {
+  extern __shared__ uint16_t sv[];  // 2^16 residues
+  constexpr uint32_t M = 0xFFFFu;
+  const int64_t vec = blockIdx.x;
+  const uint32_t *bits = p.bits + vec * 2048;
+  const int tid = threadIdx.x;
+  auto pos = [](int slot, int b0, int e) -> uint32_t {
+    const uint32_t lo = uint32_t(slot) & ((1u << b0) - 1u), hi = uint32_t(slot) >> b0;
+    return (hi << (b0 + 4)) | (uint32_t(e) << b0) | lo;
+  };
+  // G0 of the first transform, from the bitmask (16 bits per slot)
+  for (int slot = tid; slot < 4096; slot += LOC_NT) {
+    const uint32_t w = (bits[slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
+    uint32_t v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = (w >> e) & 1u;
+    wht16(v);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) sv[(slot << 4) | e] = uint16_t(v[e]);
+  }
+  __syncthreads();
+  auto round = [&](int b0, bool mul) {
+    for (int slot = tid; slot < 4096; slot += LOC_NT) {
+      uint32_t v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = sv[pos(slot, b0, e)];
+      wht16(v);
+      if (mul) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t prod = v[e] * __ldg(p.post_mul + pos(slot, b0, e));
+          v[e] = fold16(fold16(prod));
+        }
+        wht16(v);
+      }
+#pragma unroll
+      for (int e = 0; e < 16; ++e) sv[pos(slot, b0, e)] = uint16_t(v[e]);
+    }
+    __syncthreads();
+  };
+  round(4, false);
+  round(8, false);
+  round(12, true);  // end of the first transform, product, start of the second
+  round(8, false);
+  round(4, false);
+  // G0 of the second transform + epilogue
+  const uint32_t *bits_e = p.bits_e ? p.bits_e + vec * 2048 : nullptr;
+  for (int slot = tid; slot < 4096; slot += LOC_NT) {
+    uint32_t v[16];
+    const uint4 *src = reinterpret_cast<const uint4 *>(sv + (slot << 4));
+    const uint4 x0 = src[0], x1 = src[1];
+    const uint32_t w8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = (w8[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+    wht16(v);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = fold16(v[e]) == M ? 0u : fold16(v[e]);  // normalise
+    const uint32_t j0 = uint32_t(slot) << 4;
+    if (p.phi) {
+      const uint32_t er = (bits_e[slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
+      const uint4 *rxv = reinterpret_cast<const uint4 *>(p.rx + vec * p.rx_stride + j0);
+      const uint4 r0 = __ldcs(rxv), r1 = __ldcs(rxv + 1);
+      const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      uint32_t o[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        uint32_t pair = 0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int e = 2 * h + q;
+          const uint32_t r = (rw[h] >> (16 * q)) & 0xFFFFu;
+          uint32_t ph = 0;
+          if (!((er >> e) & 1u) && r) {
+            uint32_t t = uint32_t(__ldg(p.log + r)) + v[e];
+            t = t >= M ? t - M : t;
+            ph = __ldg(p.exp + t);
+          }
+          pair |= ph << (16 * q);
+        }
+        o[h] = pair;
+      }
+      uint4 *dst = reinterpret_cast<uint4 *>(p.phi + vec * p.rx_stride + j0);
+      __stcs(dst, make_uint4(o[0], o[1], o[2], o[3]));
+      __stcs(dst + 1, make_uint4(o[4], o[5], o[6], o[7]));
+      if (j0 < p.k) {
+        uint16_t *pl = p.pinv_log + vec * p.k;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint32_t j = j0 + e;
+          if (j < p.k) pl[j] = ((er >> e) & 1u) ? uint16_t(v[e] ? M - v[e] : 0u) : uint16_t(0);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const size_t idx = size_t(vec) * 65536 + j0 + e;
+        if (p.log_out) p.log_out[idx] = uint16_t(v[e]);
+        if (p.loc_out) p.loc_out[idx] = __ldg(p.exp + v[e]);
+      }
+    }
+  }
+}
+
+cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(locator16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         65536 * 2);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  locator16_kernel<<<unsigned(p.nvec), LOC_NT, 65536 * 2, s>>>(p);
+  return cudaGetLastError();
 }
 
 // decode rows from the locator logs, one row set per pattern (blockIdx.y):

@@ -145,6 +145,9 @@ size_t gather_smem_bytes(int R, const GatherParams &p);
 template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s);
 cudaError_t launch_fwht(const FwhtParams &p, cudaStream_t s);
+// whole r = 16 locator per pattern (bits, post_mul = FWHT(log), exp, and the
+// loc/log or decode epilogue fields of FwhtParams)
+cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s);
 cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const uint16_t *exp,
                                uint32_t m, uint32_t n, uint32_t k, uint16_t *pi_row,
                                uint16_t *pinv, int64_t np, cudaStream_t s);

@@ -914,18 +914,25 @@ __global__ void fwht_kernel(const __grid_constant__ FwhtParams p) {
 // values / logs, or phi = rx * Pi_bar and -log Pi' for the decode).
 constexpr int LOC_NT = 1024;
 
-__device__ __forceinline__ uint32_t fold16(uint32_t x) { return (x & 0xFFFFu) + (x >> 16); }
+// x mod (2^16 - 1) folded once: (x & 0xFFFF) + (x >> 16) = x - 65535 * (x >> 16)
+// (shift + IMAD: keeps half of the work off the integer ALU pipe)
+__device__ __forceinline__ uint32_t fold16(uint32_t x) { return x - 65535u * (x >> 16); }
 
+// 16-point WHT mod 2^16 - 1 with lazy reduction: inputs <= m, stage h adds
+// m * 2^h before subtracting (a - b + m 2^h >= 0), so values stay below
+// m * 2^(h+1) < 2^21; two folds bring them back to <= m (0xFFFF == 0).
 __device__ __forceinline__ void wht16(uint32_t (&v)[16]) {
 #pragma unroll
-  for (int h = 1; h < 16; h <<= 1)
+  for (int h = 0; h < 4; ++h)
 #pragma unroll
     for (int e = 0; e < 16; ++e)
-      if (!(e & h)) {
-        const uint32_t a = v[e], b = v[e | h];
-        v[e] = fold16(a + b);
-        v[e | h] = fold16(a + (b ^ 0xFFFFu));  // a - b mod 2^16 - 1
+      if (!(e & (1 << h))) {
+        const uint32_t a = v[e], b = v[e | (1 << h)];
+        v[e] = a + b;
+        v[e | (1 << h)] = a - b + (0xFFFFu << h);
       }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = fold16(fold16(v[e]));
 }
 
 __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant__ FwhtParams p) {

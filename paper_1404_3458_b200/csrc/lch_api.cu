@@ -426,7 +426,9 @@ int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out
   const size_t n = size_t(1) << r;
   const bool aligned = !epi || (reinterpret_cast<uintptr_t>(epi->rx) % 16 == 0 &&
                                 reinterpret_cast<uintptr_t>(epi->phi) % 16 == 0 && epi->rx_stride % 8 == 0);
-  if (r == 16 && aligned) {
+  // one CTA per pattern: used when there are enough patterns to fill the GPU
+  // (a single pattern runs faster as 4 grid-wide radix-2^8 passes)
+  if (r == 16 && aligned && np >= 32) {
     FwhtParams p;
     std::memset(&p, 0, sizeof(p));
     p.nvec = np;

@@ -129,6 +129,76 @@ struct GF {
     }
   }
 
+  // Measured alternatives (build with -DLCH_MUL_LAZY / -DLCH_MUL_LAZY2 /
+  // -DLCH_MUL_2BIT; all bit-exact, none faster than mul_acc_1 in the pass
+  // kernel: 1.41 / 1.48 / 1.47 ms vs 1.41 ms per RS(2^16,2^15) encode of 4096).
+  // Lazy-reduction multiply: u + f v accumulated as an unreduced polynomial
+  // of degree <= 2R-2 (planes R..2R-2 in h[]), so the set bits of f only
+  // XOR shifted copies of v (no per-bit x*p updates and no dependency chain
+  // through them); one reduction of h[] by the taps at the end.
+  __device__ __forceinline__ static void lazy_reduce(uint32_t (&u)[R], uint32_t (&h)[R - 1]) {
+    // x^i = x^(i-R) * TAPS for i >= R, top plane first (targets above R cascade)
+#pragma unroll
+    for (int i = 2 * R - 2; i >= R; --i) {
+      const uint32_t x = h[i - R];
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        if (!((TAPS >> s) & 1u)) continue;
+        const int t = i - R + s;
+        if (t < R)
+          u[t < R ? t : 0] ^= x;
+        else
+          h[t >= R ? t - R : 0] ^= x;
+      }
+    }
+  }
+  __device__ __forceinline__ static void mul_acc_lazy(uint32_t (&u)[R], const uint32_t (&v)[R],
+                                                      uint32_t f) {
+    uint32_t h[R - 1];
+#pragma unroll
+    for (int i = 0; i < R - 1; ++i) h[i] = 0u;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      if ((f >> t) & 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          const int i = t + b;
+          if (i < R)
+            u[i < R ? i : 0] ^= v[b];
+          else
+            h[i >= R ? i - R : 0] ^= v[b];
+        }
+      }
+    }
+    lazy_reduce(u, h);
+  }
+  // 2-bit digits: d = 3 pairs the two shifted copies in one 3-input LOP3 per plane
+  __device__ __forceinline__ static void mul_acc_lazy2(uint32_t (&u)[R], const uint32_t (&v)[R],
+                                                       uint32_t f) {
+    uint32_t h[R - 1];
+#pragma unroll
+    for (int i = 0; i < R - 1; ++i) h[i] = 0u;
+    auto pl = [&](int i) -> uint32_t & { return i < R ? u[i < R ? i : 0] : h[i >= R ? i - R : 0]; };
+#pragma unroll
+    for (int t = 0; t < ND; ++t) {
+      const uint32_t d = (f >> (2 * t)) & 3u;
+      const int o = 2 * t;
+      if (d == 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) pl(o + b) ^= v[b];
+      } else if (d == 2u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) pl(o + 1 + b) ^= v[b];
+      } else if (d == 3u) {
+        pl(o) ^= v[0];
+#pragma unroll
+        for (int b = 1; b < R; ++b) pl(o + b) = lop3_xor(pl(o + b), v[b], v[b - 1]);
+        pl(o + R) ^= v[R - 1];
+      }
+    }
+    lazy_reduce(u, h);
+  }
+
 #ifndef LCH_MUL_2BIT
   // 1-bit digits: one warp-uniform branch per bit of f (fewer taken
   // branches than the 2-bit digits below: measured 4-5% faster passes)

@@ -426,7 +426,11 @@ template <int R, uint32_t POLY>
 __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv) {
   using F = GF<R, POLY>;
   if (inv) F::xor_into(v, u);
-#ifndef LCH_MUL_2BIT
+#if defined(LCH_MUL_LAZY)
+  F::mul_acc_lazy(u, v, f);
+#elif defined(LCH_MUL_LAZY2)
+  F::mul_acc_lazy2(u, v, f);
+#elif !defined(LCH_MUL_2BIT)
   F::mul_acc_1(u, v, f);
 #else
   F::mul_acc(u, v, f);

@@ -322,15 +322,21 @@ class Timer:
         return step_ms, dict(zip([n for n, _ in phases], ph)), int(launches), clk.summary()
 
 
-def read_traffic():
+def read_profile():
+    """Per-launch DRAM traffic and ALU-pipe occupancy of the pass kernel from
+    the committed ncu capture (profiles/pass_kernel_traffic.json)."""
     tfile = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
     if os.path.exists(tfile):
         try:
             with open(tfile) as fh:
-                return json.load(fh).get("dram_bytes_per_launch")
+                return json.load(fh)
         except Exception:
-            return None
-    return None
+            return {}
+    return {}
+
+
+def read_traffic():
+    return read_profile().get("dram_bytes_per_launch")
 
 
 def base_line(args, world, value, step_ms, cfg, launches, clocks, scaling="weak"):
@@ -419,6 +425,15 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
         "roofline": roofline("pass_kernel<16,0x1100B> (encode tile pass)", per_launch_bytes,
                              per_launch_ms, peak, peak_src, read_traffic()),
     })
+    prof = read_profile()
+    if prof.get("alu_pipe_pct_per_launch"):
+        alu = prof["alu_pipe_pct_per_launch"]
+        res["compute_roofline"] = {
+            "bound": "alu", "pipe": "integer ALU (LOP3 bit-sliced GF(2^16) multiplies)",
+            "busy_frac": round(sum(alu) / len(alu) / 100.0, 3),
+            "dram_frac_same_launches": round(sum(prof.get("dram_pct_per_launch", [0])) /
+                                             max(1, len(prof.get("dram_pct_per_launch", [0]))) / 100.0, 3),
+            "source": "ncu --set full, profiles/r01_pass_kernel_full.txt"}
 
     # e2e through the public host-buffer API (lch_encode_host / lch_decode_host:
     # chunked H2D / kernels / D2H overlapped on three streams), pinned buffers

@@ -100,9 +100,15 @@ def full(path, out, traffic_out=None):
             rd = num(d["dram__bytes_read.sum"]) * scale.get(u["dram__bytes_read.sum"], 1)
             wr = num(d["dram__bytes_write.sum"]) * scale.get(u["dram__bytes_write.sum"], 1)
             tb.append(rd + wr)
+        alu = [num(d.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", 0))
+               for d in launches_]
+        dram = [num(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 0))
+                for d in launches_]
         json.dump({"source": path, "kernel": launches_[0].get("Kernel Name", "")[:80],
                    "dram_bytes_per_launch": int(sum(tb) / len(tb)),
-                   "per_launch": [int(x) for x in tb]}, open(traffic_out, "w"), indent=1)
+                   "per_launch": [int(x) for x in tb],
+                   "alu_pipe_pct_per_launch": alu, "dram_pct_per_launch": dram},
+                  open(traffic_out, "w"), indent=1)
 
 
 if __name__ == "__main__":

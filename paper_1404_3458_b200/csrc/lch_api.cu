@@ -737,11 +737,47 @@ static int transform_impl(lch_ctx *c, uint16_t *data, int64_t batch, int64_t str
   });
 }
 
+// Small GF(2^8) batches (fewer than one 1024-codeword bit-sliced group): one
+// CTA per codeword (lch_small.cu), a single launch per encode / decode.
+static bool small8_ok(const lch_ctx *c, int64_t batch, int64_t pkt) {
+  return c->t.r == 8 && c->t.poly == 0x11Du && pkt == 0 && batch > 0 && batch < GROUP &&
+         c->max_lg_h == 8 && !std::getenv("LCH_NO_SMALL8");
+}
+
+static Small8Params small8_params(const lch_ctx *c) {
+  Small8Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.max_h = int(c->t.max_h);
+  p.log = c->d_log;
+  p.exp = c->d_exp;
+  p.w_hat = c->d_w_hat;
+  p.b_prod = c->d_b_prod;
+  p.b_prod_inv = c->d_b_prod_inv;
+  p.fwht_log = c->d_fwht_log;
+  return p;
+}
+
 // Systematic encode for power-of-two k (rs.py:85-96).
 static int encode_pow2(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
                        int64_t stride_out, int64_t batch, int lg_k, int64_t pkt, cudaStream_t s) {
   const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k, nb = n / k;
   if (nb == 1) return LCH_OK;
+  if (small8_ok(c, batch, pkt)) {
+    Small8Params p = small8_params(c);
+    p.mode = 0;
+    p.k = int(k);
+    p.lg_k = lg_k;
+    p.batch = batch;
+    p.in = msg;
+    p.in_stride = stride_in;
+    p.out = parity;
+    p.out_stride = stride_out;
+    for (int64_t blk = 1; blk < nb; ++blk)
+      for (int i = 0; i < lg_k; ++i) p.hs[blk * 8 + i] = uint8_t(hs_of(c, i, uint32_t(blk * k)));
+    LCH_TRY(cu(launch_small8(p, s)));
+    c->launches++;
+    return LCH_OK;
+  }
   if (lg_k == 0) {
     // 1-point transforms are the identity: every parity symbol is the message
     const int64_t rows = pkt ? batch / pkt : batch, w = pkt ? pkt : 1;
@@ -963,6 +999,21 @@ static int decode_any(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const u
                                 cudaMemcpyDeviceToDevice, s));
   }
   if (c->max_lg_h < r) return LCH_EINVAL;  // n-point transforms (transform.py:63-64)
+  if (small8_ok(c, batch, pkt)) {
+    Small8Params p = small8_params(c);
+    p.mode = 1;
+    p.k = int(k);
+    p.batch = batch;
+    p.in = rx;
+    p.in_stride = stride_in;
+    p.out = out;
+    p.out_stride = stride_out;
+    p.bits = bits;
+    p.bits_stride = shared ? 0 : words;
+    LCH_TRY(cu(launch_small8(p, s)));
+    c->launches++;
+    return LCH_OK;
+  }
   if (!shared && !pkt) return decode_per_codeword(c, rx, stride_in, bits, out, stride_out, batch, k, s);
   const int lgo = std::max(ceil_lg(k), 1);
   const int64_t kf = int64_t(1) << lgo;

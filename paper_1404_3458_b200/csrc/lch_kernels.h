@@ -139,6 +139,23 @@ struct FwhtParams {
   uint32_t k;
 };
 
+// Small-codeword GF(2^8) codec (lch_small.cu): one CTA per codeword.
+struct Small8Params {
+  int mode;                 // 0 encode (power-of-two k), 1 decode (any k)
+  int k, lg_k, max_h;
+  int64_t batch;
+  const uint16_t *in;       // message [batch][k] or received [batch][256]
+  int64_t in_stride;
+  uint16_t *out;            // parity [batch][256 - k] or message [batch][k]
+  int64_t out_stride;
+  const uint32_t *bits;     // decode: erasure bitmask words, 8 per pattern
+  int64_t bits_stride;      // 0 = one shared pattern
+  const uint16_t *log, *exp, *w_hat, *b_prod, *b_prod_inv;
+  const uint32_t *fwht_log;
+  uint8_t hs[256 * 8];      // encode: W^_i(blk * k) per parity block and level
+};
+cudaError_t launch_small8(const Small8Params &p, cudaStream_t s);
+
 template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s);
 size_t gather_smem_bytes(int R, const GatherParams &p);

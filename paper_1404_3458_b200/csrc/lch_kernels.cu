@@ -426,15 +426,19 @@ template <int R, uint32_t POLY>
 __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv) {
   using F = GF<R, POLY>;
   if (inv) F::xor_into(v, u);
+  // zero factors (block 0 of every level at shift 0, transform.py:154-161)
+  // are a warp-uniform skip
+  if (f) {
 #if defined(LCH_MUL_LAZY)
-  F::mul_acc_lazy(u, v, f);
+    F::mul_acc_lazy(u, v, f);
 #elif defined(LCH_MUL_LAZY2)
-  F::mul_acc_lazy2(u, v, f);
+    F::mul_acc_lazy2(u, v, f);
 #elif !defined(LCH_MUL_2BIT)
-  F::mul_acc_1(u, v, f);
+    F::mul_acc_1(u, v, f);
 #else
-  F::mul_acc(u, v, f);
+    F::mul_acc(u, v, f);
 #endif
+  }
   if (!inv) F::xor_into(v, u);
 }
 
@@ -447,11 +451,13 @@ __device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R],
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);
   }
+  if (f) {
 #ifndef LCH_MUL_2BIT
-  F::mul_acc2_1(u0, v0, u1, v1, f);
+    F::mul_acc2_1(u0, v0, u1, v1, f);
 #else
-  F::mul_acc2(u0, v0, u1, v1, f);
+    F::mul_acc2(u0, v0, u1, v1, f);
 #endif
+  }
   if (!inv) {
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);

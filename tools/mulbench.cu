@@ -1,4 +1,4 @@
-// Microbenchmark: throughput of the bit-sliced Horner multiply (warp-uniform
+// Microbenchmark: throughput of the bit-sliced multiply (GF::mul_acc_1) (warp-uniform
 // factors) with W words per lane sharing each factor.  Experiments only.
 #include <cstdint>
 #include <cstdio>
@@ -14,13 +14,11 @@ __global__ void __launch_bounds__(256) k(const uint32_t *fac, uint32_t *out, int
   for (int it = 0; it < iters; ++it) {
     const uint32_t f = fac[(blockIdx.x * 8 + warp + it * 7) & 4095];
     if (W == 1) {
-      uint32_t t[16];
-      F::mul(t, v[0], f);
-      for (int b = 0; b < 16; ++b) { u[0][b] ^= t[b]; v[0][b] ^= u[0][b]; }
+      F::mul_acc_1(u[0], v[0], f);
+      for (int b = 0; b < 16; ++b) v[0][b] ^= u[0][b];
     } else {
-      uint32_t t0[16], t1[16];
-      F::mul2(t0, t1, v[0], v[W - 1], f);
-      for (int b = 0; b < 16; ++b) { u[0][b] ^= t0[b]; v[0][b] ^= u[0][b]; u[W-1][b] ^= t1[b]; v[W-1][b] ^= u[W-1][b]; }
+      F::mul_acc2_1(u[0], v[0], u[W - 1], v[W - 1], f);
+      for (int b = 0; b < 16; ++b) { v[0][b] ^= u[0][b]; v[W-1][b] ^= u[W-1][b]; }
     }
   }
   uint32_t x = 0;

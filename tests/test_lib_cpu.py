@@ -135,3 +135,60 @@ def test_no_cpu_fallback():
     # the raw ABI refuses too (no device): LCH_ECUDA
     rc = _lib.lib.lch_forward(bt.ctx.handle, None, 1, 4, 2, 0, 0, None)
     assert rc == _lib.LCH_ECUDA
+
+
+def test_general_k_and_packet_validation_before_device():
+    """lch_encode_k / lch_decode_k / host pipeline argument checks run before
+    any device access (so they hold on CPU-only hosts)."""
+    import ctypes
+    ft = lch.tables_for(8)
+    bt = lch.build_basis_tables(ft, 256)
+    h = bt.ctx.handle
+    L = _lib.lib
+    EINVAL = _lib.LCH_EINVAL
+    buf = (ctypes.c_uint16 * 4096)()
+    p = ctypes.addressof(buf)
+    p16 = p + (16 - p % 16) % 16  # 16-byte aligned
+    # k outside [1, n]
+    assert L.lch_encode_k(h, p16, 256, p16, 256, 1, 0, 0, None) == EINVAL
+    assert L.lch_encode_k(h, p16, 256, p16, 256, 1, 257, 0, None) == EINVAL
+    # strides too small
+    assert L.lch_encode_k(h, p16, 99, p16, 156, 1, 100, 0, None) == EINVAL
+    assert L.lch_encode_k(h, p16, 100, p16, 155, 1, 100, 0, None) == EINVAL
+    # packet_len not a multiple of 1024, batch not a multiple of packet_len, misaligned
+    assert L.lch_encode_k(h, p16, 128, p16, 128, 1000, 128, 1000, None) == EINVAL
+    assert L.lch_encode_k(h, p16, 128, p16, 128, 1500, 128, 1024, None) == EINVAL
+    assert L.lch_encode_k(h, p16 + 2, 128, p16, 128, 1024, 128, 1024, None) == EINVAL
+    # decode: k range, strides, missing bitmask
+    assert L.lch_decode_k(h, p16, 256, p16, 1, p16, 128, 1, 0, 0, None, None) == EINVAL
+    assert L.lch_decode_k(h, p16, 255, p16, 1, p16, 128, 1, 128, 0, None, None) == EINVAL
+    assert L.lch_decode_k(h, p16, 256, None, 1, p16, 128, 1, 128, 0, None, None) == EINVAL
+    # host pipeline
+    assert L.lch_encode_host(h, None, 128, p16, 128, 1, 128, 0, 0, None) == EINVAL
+    assert L.lch_decode_host(h, p16, 256, None, 1, p16, 128, 1, 128, 0, 0, None) == EINVAL
+    assert L.lch_decode_host(h, p16, 256, p16, 1, p16, 128, 1, 128, 1000, 0, None) == EINVAL
+    assert L.lch_set_scratch_limit(h, 0) == EINVAL
+    with pytest.raises(ValueError):
+        lch.StripeCodec(bt, 0, 1024)
+    with pytest.raises(ValueError):
+        lch.StripeCodec(bt, 128, 1000)
+
+
+def test_host_pipeline_too_many_from_host_counts():
+    """lch_decode_host counts erasures from the host bitmask (rs.py:121-123)
+    before any device work."""
+    import ctypes
+    ft = lch.tables_for(8)
+    bt = lch.build_basis_tables(ft, 256)
+    bits = np.zeros(8, np.uint32)
+    bits[:5] = 0xFFFFFFFF  # 160 erasures > n - k = 128
+    rx = np.zeros((1, 256), np.uint16)
+    out = np.zeros((1, 128), np.uint16)
+    rc = _lib.lib.lch_decode_host(bt.ctx.handle, rx.ctypes.data, 256, bits.ctypes.data, 1,
+                                  out.ctypes.data, 128, 1, 128, 0, 0, None)
+    assert rc in (_lib.LCH_ETOOMANY, _lib.LCH_ECUDA)
+    if not _lib.cuda_ok():
+        # ensure_device() runs first on a CPU-only host
+        assert rc == _lib.LCH_ECUDA
+    with pytest.raises(Exception):
+        lch.BatchCodec(lch.CodeParams(8, 128), bt).decode(rx, set(range(129)))

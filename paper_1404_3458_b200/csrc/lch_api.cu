@@ -328,62 +328,32 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
   const int ngroups = int((batch + GROUP - 1) / GROUP);
   std::sort(bits.begin(), bits.end());
   if (special >= 0) bits.erase(std::remove(bits.begin(), bits.end(), special), bits.end());
-  // shared-memory need of a tile over `grp` (+ the special bit), one lane-word
-  auto need = [&](const std::vector<int> &grp, bool first) {
-    int nlow = 0;
-    const int nb = int(grp.size()) + (first && special >= 0 ? 1 : 0);
-    for (int b : grp) nlow += b < lgH_out;
-    const bool has_tin = !first || t_in;
-    return ((size_t(1) << nb) + (has_tin ? (size_t(1) << nlow) : 0)) * R * 4;
-  };
-  // greedy split (largest tiles), then the same number of passes with
-  // balanced sizes so no pass degenerates into tiny tiles
-  auto split = [&](size_t cap) {
-    std::vector<std::vector<int>> out;
-    size_t i = 0;
-    bool first = true;
-    while (i < bits.size()) {
-      std::vector<int> grp;
-      const size_t room = std::min<size_t>(cap, GMAXB - (first && special >= 0 ? 1 : 0));
-      while (i < bits.size() && grp.size() < room) {
-        grp.push_back(bits[i]);
-        if (need(grp, first) > GATHER_SMEM_MAX) {
-          grp.pop_back();
-          break;
-        }
-        ++i;
-      }
-      if (grp.empty()) break;
-      out.push_back(grp);
-      first = false;
-    }
-    return out;
-  };
-  auto groups = split(GMAXB);
-  if (groups.size() > 1) {
-    const size_t per = (bits.size() + groups.size() - 1) / groups.size();
-    auto bal = split(per);
-    if (bal.size() == groups.size()) groups = bal;
+  // shared memory holds the y tile over the summed bits (one lane-word)
+  auto need = [&](size_t nb) { return (size_t(1) << nb) * R * 4; };
+  size_t maxb = 0;
+  while (maxb < size_t(GMAXB) && need(maxb + 1) <= GATHER_SMEM_MAX) ++maxb;
+  // fewest passes, then balanced sizes so no pass degenerates into tiny tiles
+  const size_t npass = bits.empty() ? (special >= 0 ? 1 : 0) : (bits.size() + maxb - 1) / maxb;
+  std::vector<std::vector<int>> groups;
+  for (size_t i = 0, pi = 0; pi < npass; ++pi) {
+    const size_t sz = (bits.size() - i + (npass - pi) - 1) / (npass - pi);
+    groups.emplace_back(bits.begin() + long(i), bits.begin() + long(i + sz));
+    i += sz;
   }
-  if (groups.empty() && special >= 0) groups.push_back({});
   bool first = true;
   for (auto grp : groups) {
     GatherParams p;
     std::memset(&p, 0, sizeof(p));
-    const size_t nd = need(grp, first);
-    p.sb = -1;
-    if (first && special >= 0) {
-      grp.push_back(special);
-      std::sort(grp.begin(), grp.end());
-      p.sb = int(std::find(grp.begin(), grp.end(), special) - grp.begin());
-      p.c = cconst;
-    }
+    p.sb = (first && special >= 0) ? special : -1;
+    p.c = cconst;
     p.nbits = int(grp.size());
-    // lane-words per CTA: >= ~2048 position-words per CTA within the smem budget
+    // lane-words per CTA: ~1024 position-words per CTA within the smem budget
     p.lwpc = 0;
-    while (p.lwpc < 5 && (nd << (p.lwpc + 1)) <= GATHER_SMEM_MAX && (p.nbits + p.lwpc) < 11) ++p.lwpc;
+    while (p.lwpc < 5 && (need(grp.size()) << (p.lwpc + 1)) <= GATHER_SMEM_MAX && (p.nbits + p.lwpc) < 10)
+      ++p.lwpc;
     p.lgH_in = lgH_in;
     p.lgH_out = lgH_out;
+    std::vector<int> tile_and_special = grp;
     fill_bits(grp, lgH_in, p.bits, p.nnb, p.nbit);
     p.y = y;
     p.t_in = first ? t_in : t;

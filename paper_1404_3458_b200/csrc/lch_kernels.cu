@@ -765,10 +765,13 @@ constexpr int GNT = 512;  // gather threads per CTA
 
 // Tile bits are sorted, so the tile positions below 2^lgH_out (the outputs)
 // are exactly q < 2^nlow with nlow = #tile bits below lgH_out (base < 2^lgH_out).
-// A CTA covers one tile of 2^nbits positions for 2^lwpc consecutive lane-words
-// (small tiles take more words so every CTA moves >= ~64 KB).
+// Only the y values over the summed tile bits are staged in shared memory
+// (each is read by up to nbits outputs); T_in and the special bit's partner
+// y_(j | 2^special) are read once per output straight from global memory.
+// A CTA covers one tile for 2^lwpc consecutive lane-words (small tiles take
+// more words so every CTA moves a useful amount of data).
 template <int R, uint32_t POLY>
-__global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ GatherParams p) {
+__global__ void __launch_bounds__(GNT, 2) gather_kernel(const __grid_constant__ GatherParams p) {
   constexpr int CH = R / 4;  // 16-byte chunks of one lane-word
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
@@ -780,7 +783,7 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
   const int lw = p.lwpc, WPC = 1 << lw;
   const int wblocks = 32 >> lw;
   const int g = blockIdx.y / wblocks, w0 = (blockIdx.y - g * wblocks) * WPC;
-  uint4 *ytile = smem, *ttile = smem + (np << lw) * CH;
+  uint4 *ytile = smem;
   const uint32_t t = blockIdx.x;
   uint32_t base = 0;
   for (int i = 0; i < p.nnb; ++i) base |= ((t >> i) & 1u) << p.nbit[i];
@@ -793,20 +796,12 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
   };
   // e = q * WPC + word offset; the chunk swizzle keeps quarter-warps conflict-free
   auto slot = [](int e, int c) { return e * CH + (c ^ ((e >> 1) & (CH - 1))); };
-  // stage lane-words [w0, w0 + WPC) of every tile position (and of T_in at the outputs)
   const uint4 *src = p.y + ((size_t(g) << p.lgH_in) * U4);
   for (int idx = tid; idx < (np << lw) * CH; idx += GNT) {
     const int e = idx / CH, c = idx - e * CH;
     const int q = e >> lw, wl = e & (WPC - 1);
     cp_async16(ytile + slot(e, c), src + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w0 + wl, c));
   }
-  const uint4 *tin = p.t_in ? p.t_in + ((size_t(g) << p.lgH_out) * U4) : nullptr;
-  if (tin)
-    for (int idx = tid; idx < (nout << lw) * CH; idx += GNT) {
-      const int e = idx / CH, c = idx - e * CH;
-      const int q = e >> lw, wl = e & (WPC - 1);
-      cp_async16(ttile + slot(e, c), tin + size_t(pos_of(q)) * U4 + Blk<R>::chunk(w0 + wl, c));
-    }
   cp_async_wait_all();
   __syncthreads();
   auto ld = [&](const uint4 *tile, int e, uint32_t (&v)[R]) {
@@ -819,34 +814,45 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
       v[4 * c + 3] = x.w;
     }
   };
+  auto ldg = [&](const uint4 *blk, int w, uint32_t (&v)[R]) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const uint4 x = __ldcs(blk + Blk<R>::chunk(w, c));
+      v[4 * c + 0] = x.x;
+      v[4 * c + 1] = x.y;
+      v[4 * c + 2] = x.z;
+      v[4 * c + 3] = x.w;
+    }
+  };
+  const uint4 *tin = p.t_in ? p.t_in + ((size_t(g) << p.lgH_out) * U4) : nullptr;
   uint4 *tout = p.t_out + ((size_t(g) << p.lgH_out) * U4);
   for (int e = tid; e < (nout << lw); e += GNT) {
     const int q = e >> lw, wl = e & (WPC - 1);
+    const uint32_t pos = pos_of(q);
     uint32_t acc[R];
     if (tin) {
-      ld(ttile, e, acc);
+      ldg(tin + size_t(pos) * U4, w0 + wl, acc);
     } else {
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] = 0u;
     }
     for (int m = 0; m < p.nbits; ++m) {
-      if (m == p.sb || ((q >> m) & 1)) continue;
+      if ((q >> m) & 1) continue;
       uint32_t x[R];
       ld(ytile, e | (1 << (m + lw)), x);
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= x[b];
     }
-    if (p.sb >= 0) {  // q < nout has the special (top) bit clear
+    if (p.sb >= 0) {  // the output has the special (top) bit clear
       uint32_t x[R], z[R], cz[R];
+      ldg(src + size_t(pos | (1u << p.sb)) * U4, w0 + wl, z);
       ld(ytile, e, x);
-      ld(ytile, e | (1 << (p.sb + lw)), z);
 #pragma unroll
       for (int b = 0; b < R; ++b) z[b] ^= x[b];
       GF<R, POLY>::mul(cz, z, p.c);  // c is a kernel constant: uniform
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= cz[b];
     }
-    const uint32_t pos = pos_of(q);
 #pragma unroll
     for (int c = 0; c < CH; ++c)
       tout[size_t(pos) * U4 + Blk<R>::chunk(w0 + wl, c)] =
@@ -855,9 +861,7 @@ __global__ void __launch_bounds__(GNT) gather_kernel(const __grid_constant__ Gat
 }
 
 size_t gather_smem_bytes(int R, const GatherParams &p) {
-  int nlow = 0;
-  while (nlow < p.nbits && p.bits[nlow] < p.lgH_out) ++nlow;
-  return (((size_t(1) << p.nbits) + (p.t_in ? (size_t(1) << nlow) : 0)) * R * 4) << p.lwpc;
+  return ((size_t(1) << p.nbits) * R * 4) << p.lwpc;
 }
 
 // Walsh-Hadamard transform over Z_mod, bits [b0, b0 + tb) of each vector

@@ -104,11 +104,11 @@ struct PassParams {
 //                  + c * (y[j] + y[j | 2^bits[sb]])   (if sb >= 0, bit clear)
 // for j < 2^lgH_out.  One CTA per (tile, group, lane-word).
 constexpr int GMAXB = 11;
-constexpr size_t GATHER_SMEM_MAX = 200 * 1024;
+constexpr size_t GATHER_SMEM_MAX = 96 * 1024;  // 2 CTAs per SM
 struct GatherParams {
   int nbits;
   int bits[GMAXB];
-  int sb;                // index into bits[] of the special bit, or -1
+  int sb;                // the special (top) position bit, not a tile bit, or -1
   uint32_t c;            // constant for the special bit
   int lgH_in, lgH_out;
   int nnb;

@@ -406,12 +406,9 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
       const uint32_t f = __shfl_sync(
           0xffffffffu, uint32_t(__ldg(ops[o].table + trow * ops[o].tab_stride + (base | tpos[q]))), 0);
       uint32_t acc[R];
-      if (f) {
-        F::mul(acc, v, f);
-      } else {
 #pragma unroll
-        for (int b = 0; b < R; ++b) acc[b] = 0u;
-      }
+      for (int b = 0; b < R; ++b) acc[b] = 0u;
+      if (f) F::mul_acc_1(acc, v, f);
 #pragma unroll
       for (int b = 0; b < R; ++b) v[b] = acc[b];
     }

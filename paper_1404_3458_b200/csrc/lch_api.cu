@@ -728,11 +728,16 @@ static Small8Params small8_params(const lch_ctx *c) {
 }
 
 // Systematic encode for power-of-two k (rs.py:85-96).
+// Code length 2^lg_n (<= the field size): parity blocks at shifts k, 2k, ...
+// (a sub-code of a longer one evaluates the same polynomials on its first
+// 2^lg_n points, so the shift constants are the field's).
 static int encode_pow2(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
-                       int64_t stride_out, int64_t batch, int lg_k, int64_t pkt, cudaStream_t s) {
-  const int64_t n = int64_t(c->t.order), k = int64_t(1) << lg_k, nb = n / k;
+                       int64_t stride_out, int64_t batch, int lg_k, int64_t pkt, cudaStream_t s,
+                       int lg_n = -1) {
+  if (lg_n < 0) lg_n = c->t.r;
+  const int64_t k = int64_t(1) << lg_k, nb = (int64_t(1) << lg_n) / k;
   if (nb == 1) return LCH_OK;
-  if (small8_ok(c, batch, pkt)) {
+  if (small8_ok(c, batch, pkt) && lg_n == c->t.r) {
     Small8Params p = small8_params(c);
     p.mode = 0;
     p.k = int(k);
@@ -846,6 +851,93 @@ static int encode_tables(lch_ctx *c, int64_t k, const uint16_t *&pi_row, const u
   return LCH_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Systematic encode for any k ("a first-class codec"): the
+// codeword is the evaluation of the degree < k interpolant f of the message
+// (the code of SURVEY H6), computed by recursion on the binary expansion of k
+// instead of erasure decoding.  With h = n/2 and k > h, f = A + X_h R where
+// deg A < h: X_h vanishes on [0, h) and is 1 on [h, n) (normalised subspace
+// polynomial), so A interpolates m on [0, h), its values on [h, n) are the
+// parity of the power-of-two code (2h, h) (rs.encode), and R is the degree
+// < k - h interpolant of m - A on [h, k), a smaller instance of the same
+// problem on the coset [h, n).  Parity = A + R on [k, n).  For k < h not a
+// power of two the first 2^ceil(lg k) values are completed recursively and
+// then encoded as a power-of-two code.  Every step is a power-of-two encode
+// (the fused pass-kernel plans) or an XOR of arrays.
+
+struct View {
+  uint16_t *p;
+  int64_t s;  // row stride (row layout) or positions per stripe group (packet layout)
+};
+
+static View vsub(View v, int64_t j0, int64_t pkt) { return View{at_pos(v.p, j0, pkt), v.s}; }
+
+static int vtemp(Scratch &sc, int64_t batch, int64_t len, View &v) {
+  LCH_TRY(sc.alloc(v.p, size_t(std::max<int64_t>(batch * len, 1))));
+  v.s = len;
+  return LCH_OK;
+}
+
+// out = a ^ b (b.p == nullptr: copy) over positions [0, len)
+static int vxor(lch_ctx *c, View out, View a, View b, int64_t batch, int64_t len, int64_t pkt,
+                cudaStream_t s) {
+  if (len <= 0 || batch <= 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_xor_views(out.p, out.s, a.p, a.s, b.p, b.s, batch, len, pkt, s));
+}
+
+static int ilog2(int64_t x) {
+  int l = 0;
+  while ((int64_t(1) << (l + 1)) <= x) ++l;
+  return l;
+}
+
+// values on [K, np) of the degree < K interpolant of v on [0, K)
+static int solve_interp(lch_ctx *c, View v, View out, int64_t batch, int64_t np, int64_t K,
+                        int64_t pkt, cudaStream_t s, Scratch &sc) {
+  if (K >= np) return LCH_OK;
+  if ((K & (K - 1)) == 0)
+    return encode_pow2(c, v.p, v.s, out.p, out.s, batch, ilog2(K), pkt, s, ilog2(np));
+  const int64_t h = np / 2;
+  if (K > h) {
+    View a{}, diff{}, sub{};
+    LCH_TRY(vtemp(sc, batch, h, a));
+    LCH_TRY(encode_pow2(c, v.p, v.s, a.p, a.s, batch, ilog2(h), pkt, s, ilog2(np)));  // A on [h, np)
+    LCH_TRY(vtemp(sc, batch, K - h, diff));
+    LCH_TRY(vxor(c, diff, vsub(v, h, pkt), a, batch, K - h, pkt, s));  // m - A on [h, K)
+    LCH_TRY(vtemp(sc, batch, np - K, sub));
+    LCH_TRY(solve_interp(c, diff, sub, batch, h, K - h, pkt, s, sc));  // R on [K, np)
+    return vxor(c, out, vsub(a, K - h, pkt), sub, batch, np - K, pkt, s);
+  }
+  int64_t t = 1;
+  while (t < K) t <<= 1;
+  View full{};
+  LCH_TRY(vtemp(sc, batch, t, full));
+  LCH_TRY(vxor(c, full, v, View{nullptr, 0}, batch, K, pkt, s));
+  LCH_TRY(solve_interp(c, v, vsub(full, K, pkt), batch, t, K, pkt, s, sc));
+  LCH_TRY(vxor(c, out, vsub(full, K, pkt), View{nullptr, 0}, batch, t - K, pkt, s));
+  if (t < np)
+    LCH_TRY(encode_pow2(c, full.p, full.s, at_pos(out.p, t - K, pkt), out.s, batch, ilog2(t), pkt, s,
+                        ilog2(np)));
+  return LCH_OK;
+}
+
+static int encode_general(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
+                          int64_t stride_out, int64_t batch, int64_t k, int64_t pkt, cudaStream_t s) {
+  const int64_t n = int64_t(c->t.order);
+  // temporaries: ~2n symbols per lane at the top level of the recursion
+  const int64_t ch = chunk_lanes(c, batch, pkt, size_t(4 * n));
+  for (int64_t b0 = 0; b0 < batch; b0 += ch) {
+    const int64_t nb = std::min(ch, batch - b0);
+    const int64_t off_in = pkt ? (b0 / pkt) * stride_in * pkt : b0 * stride_in;
+    const int64_t off_out = pkt ? (b0 / pkt) * stride_out * pkt : b0 * stride_out;
+    Scratch sc(s);
+    LCH_TRY(solve_interp(c, View{const_cast<uint16_t *>(msg) + off_in, stride_in},
+                         View{parity + off_out, stride_out}, nb, n, k, pkt, s, sc));
+  }
+  return LCH_OK;
+}
+
 static int encode_any(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
                       int64_t stride_out, int64_t batch, int64_t k, int64_t pkt, void *stream) {
   if (!c || batch < 0) return LCH_EINVAL;
@@ -861,6 +953,9 @@ static int encode_any(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint16
   if (batch == 0 || k == n) return LCH_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (pow2) return encode_pow2(c, msg, stride_in, parity, stride_out, batch, ceil_lg(k), pkt, s);
+  if (!std::getenv("LCH_ENCODE_BY_DECODE"))
+    return encode_general(c, msg, stride_in, parity, stride_out, batch, k, pkt, s);
+  // encode-by-erasure-decode (same codeword; kept for cross-checks)
   const uint16_t *pi_row = nullptr, *pinv = nullptr;
   LCH_TRY(encode_tables(c, k, pi_row, pinv, s));
   RawIO in_io = make_io(msg, stride_in, pkt);

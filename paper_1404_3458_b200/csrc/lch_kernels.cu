@@ -1215,6 +1215,37 @@ cudaError_t launch_gen_symbols(uint64_t seed, uint64_t cw0, int64_t batch, int64
   return cudaGetLastError();
 }
 
+__global__ void xor_views_kernel(uint16_t *out, int64_t so, const uint16_t *a, int64_t sa,
+                                 const uint16_t *b, int64_t sb, int64_t batch, int64_t len,
+                                 int64_t pkt) {
+  const int64_t total = batch * len;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t oo, oa, ob;
+    if (pkt) {
+      const int64_t t = i % pkt, rest = i / pkt, j = rest % len, g = rest / len;
+      oo = (g * so + j) * pkt + t;
+      oa = (g * sa + j) * pkt + t;
+      ob = (g * sb + j) * pkt + t;
+    } else {
+      const int64_t r = i / len, j = i - r * len;
+      oo = r * so + j;
+      oa = r * sa + j;
+      ob = r * sb + j;
+    }
+    out[oo] = b ? uint16_t(a[oa] ^ b[ob]) : a[oa];
+  }
+}
+
+cudaError_t launch_xor_views(uint16_t *out, int64_t so, const uint16_t *a, int64_t sa,
+                             const uint16_t *b, int64_t sb, int64_t batch, int64_t len, int64_t pkt,
+                             cudaStream_t s) {
+  const int64_t total = batch * len;
+  const int blocks = int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
+  xor_views_kernel<<<blocks, 256, 0, s>>>(out, so, a, sa, b, sb, batch, len, pkt);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gen_packets(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
                                uint32_t mask, uint16_t *out, int64_t npos, int64_t pkt,
                                cudaStream_t s) {

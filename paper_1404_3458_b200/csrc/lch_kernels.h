@@ -168,6 +168,12 @@ cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s);
 cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const uint16_t *exp,
                                uint32_t m, uint32_t n, uint32_t k, uint16_t *pi_row,
                                uint16_t *pinv, int64_t np, cudaStream_t s);
+// out = a ^ b (or a when b is null) over positions [0, len) of `batch` lanes,
+// row (pkt = 0, strides = row strides) or packet layout (strides = positions
+// per stripe group); out may alias a or b.
+cudaError_t launch_xor_views(uint16_t *out, int64_t so, const uint16_t *a, int64_t sa,
+                             const uint16_t *b, int64_t sb, int64_t batch, int64_t len, int64_t pkt,
+                             cudaStream_t s);
 cudaError_t launch_gen_packets(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
                                uint32_t mask, uint16_t *out, int64_t npos, int64_t pkt,
                                cudaStream_t s);

@@ -255,3 +255,30 @@ def test_chunked_equals_unchunked(lch, bt16):
         np.testing.assert_array_equal(f_chunk, host(b))
     finally:
         set_scratch_limit(bt16, 4 << 30)
+
+
+@pytest.mark.parametrize("r,k,B", [(8, 100, 1500), (8, 200, 2048), (16, 49152, 1024), (16, 40000, 1024)])
+def test_general_encoder_equals_encode_by_decode(lch, bt8, bt16, r, k, B):
+    """The recursive systematic encoder and the erasure-decode encoder give the
+    same codeword (both are the degree < k interpolant)."""
+    import os
+    import torch
+    from paper_1404_3458_b200 import _lib
+    bt = bt8 if r == 8 else bt16
+    n = 1 << r
+    msg = dev(O.gen_symbols(SEED + k, r, 0, B, k))
+    outs = []
+    for env in (None, "1"):
+        if env:
+            os.environ["LCH_ENCODE_BY_DECODE"] = env
+        try:
+            par = torch.empty((B, n - k), dtype=torch.int16, device="cuda")
+            _lib.check(_lib.lib.lch_encode_k(bt.ctx.handle, msg.data_ptr(), k, par.data_ptr(), n - k, B, k,
+                                             0, _lib.stream_ptr()))
+            outs.append(host(par))
+        finally:
+            os.environ.pop("LCH_ENCODE_BY_DECODE", None)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    if r == 16:
+        m0 = host(msg)[0]
+        np.testing.assert_array_equal(outs[0][0], O.Oracle(16).encode_any(k, m0)[k:])

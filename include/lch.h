@@ -165,6 +165,26 @@ int lch_decode_host(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride_in,
  * bit-sliced intermediates exceed it are processed in lane chunks. */
 int lch_set_scratch_limit(lch_ctx *ctx, uint64_t bytes);
 
+/* Shard-file layouts (reference shardfile.py:16-20,109-140).  A file of
+ * `len` bytes is stripes [S][k] of r/8-byte little-endian symbols, zero
+ * padded (S = ceil(len / (k r/8))); shard j holds symbol j of every stripe.
+ * The codec's packet layout with one stripe group and lanes = stripes,
+ * packets [positions][packet_len] (packet_len >= S, lanes >= S zero), is the
+ * shard layout:
+ *   lch_stripes_to_packets   file bytes -> message packets [k][packet_len]
+ *   lch_packets_to_stripes   message packets -> file bytes (cut to len)
+ *   lch_payload_to_packets   shard payloads [rows][S * r/8] -> packets
+ *   lch_packets_to_payload   packets -> shard payloads
+ * All pointers are device pointers. */
+int lch_stripes_to_packets(lch_ctx *ctx, const uint8_t *file, int64_t len, int r, int64_t k,
+                           uint16_t *packets, int64_t packet_len, void *stream);
+int lch_packets_to_stripes(lch_ctx *ctx, const uint16_t *packets, int64_t packet_len, int r,
+                           int64_t k, uint8_t *file, int64_t len, void *stream);
+int lch_payload_to_packets(lch_ctx *ctx, const uint8_t *payload, int64_t rows, int64_t stripes,
+                           int r, uint16_t *packets, int64_t packet_len, void *stream);
+int lch_packets_to_payload(lch_ctx *ctx, const uint16_t *packets, int64_t packet_len, int64_t rows,
+                           int64_t stripes, int r, uint8_t *payload, void *stream);
+
 /* Seeded counter-based inputs (oracle/lch_oracle.c orc_key):
  * out[b][j] = key(seed, cw0 + b, j) & (2^r - 1), row-major with row_stride. */
 int lch_gen_symbols(lch_ctx *ctx, uint64_t seed, uint64_t cw0, int64_t batch,

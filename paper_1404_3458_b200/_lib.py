@@ -59,6 +59,10 @@ def _load() -> ctypes.CDLL:
         "lch_decode_host": ([P, P, i64, P, i32, P, i64, i64, i64, i64, i64, P], i32),
         "lch_gen_symbols": ([P, u64, u64, i64, i64, P, i64, P], i32),
         "lch_gen_packets": ([P, u64, u64, i64, i64, P, i64, i64, P], i32),
+        "lch_stripes_to_packets": ([P, P, i64, i32, i64, P, i64, P], i32),
+        "lch_packets_to_stripes": ([P, P, i64, i32, i64, P, i64, P], i32),
+        "lch_payload_to_packets": ([P, P, i64, i64, i32, P, i64, P], i32),
+        "lch_packets_to_payload": ([P, P, i64, i64, i64, i32, P, P], i32),
         "lch_gen_keys": ([P, u64, u64, i64, i64, P, P], i32),
         "lch_launch_count": ([P], i64),
     }

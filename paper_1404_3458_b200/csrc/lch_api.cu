@@ -1421,6 +1421,53 @@ int lch_gen_packets(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int6
                                static_cast<cudaStream_t>(stream)));
 }
 
+// ---- shard-file layouts (shardfile.py:109-140) ----------------------------
+
+int lch_stripes_to_packets(lch_ctx *c, const uint8_t *file, int64_t len, int r, int64_t k,
+                           uint16_t *packets, int64_t packet_len, void *stream) {
+  if (!c || len < 0 || (r != 8 && r != 16) || k < 1 || packet_len < 1 || (len && !file) || !packets)
+    return LCH_EINVAL;
+  const int w = r / 8;
+  const int64_t S = (len + k * w - 1) / (k * w);
+  if (packet_len < S) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  c->launches++;
+  return cu(launch_stripes_to_packets(file, len, w, k, S, packets, packet_len,
+                                      static_cast<cudaStream_t>(stream)));
+}
+
+int lch_packets_to_stripes(lch_ctx *c, const uint16_t *packets, int64_t packet_len, int r, int64_t k,
+                           uint8_t *file, int64_t len, void *stream) {
+  if (!c || len < 0 || (r != 8 && r != 16) || k < 1 || packet_len < 1 || !packets || (len && !file))
+    return LCH_EINVAL;
+  const int w = r / 8;
+  if (packet_len < (len + k * w - 1) / (k * w)) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (len == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_packets_to_stripes(packets, packet_len, k, w, file, len, static_cast<cudaStream_t>(stream)));
+}
+
+int lch_payload_to_packets(lch_ctx *c, const uint8_t *payload, int64_t rows, int64_t stripes, int r,
+                           uint16_t *packets, int64_t packet_len, void *stream) {
+  if (!c || rows < 0 || stripes < 0 || (r != 8 && r != 16) || packet_len < stripes || !packets) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (rows == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_payload_packets(payload, packets, rows, stripes, packet_len, r / 8, 1, nullptr, nullptr,
+                                   static_cast<cudaStream_t>(stream)));
+}
+
+int lch_packets_to_payload(lch_ctx *c, const uint16_t *packets, int64_t packet_len, int64_t rows,
+                           int64_t stripes, int r, uint8_t *payload, void *stream) {
+  if (!c || rows < 0 || stripes < 0 || (r != 8 && r != 16) || packet_len < stripes || !packets) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (rows == 0 || stripes == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_payload_packets(nullptr, nullptr, rows, stripes, packet_len, r / 8, 0, payload, packets,
+                                   static_cast<cudaStream_t>(stream)));
+}
+
 int lch_gen_keys(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int64_t len, int64_t *keys,
                  void *stream) {
   if (!c || batch < 0 || len < 0) return LCH_EINVAL;

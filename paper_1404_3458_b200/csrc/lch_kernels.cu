@@ -1246,6 +1246,82 @@ cudaError_t launch_xor_views(uint16_t *out, int64_t so, const uint16_t *a, int64
   return cudaGetLastError();
 }
 
+// Shard-file layouts (reference shardfile.py:16-20,109-140): a file is
+// stripes [S][k] of w-byte little-endian symbols (zero padded); shard j holds
+// symbol j of every stripe.  The codec's packet layout [positions][P] (one
+// stripe group, lanes = stripes) is exactly the shard layout.
+__global__ void stripes_to_packets_kernel(const uint8_t *bytes, int64_t len, int w, int64_t k,
+                                          int64_t S, uint16_t *pk, int64_t P) {
+  const int64_t total = k * P;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = i / P, sidx = i - j * P;
+    uint32_t v = 0;
+    if (sidx < S) {
+      const int64_t off = (sidx * k + j) * w;
+      if (off < len) v = bytes[off];
+      if (w == 2 && off + 1 < len) v |= uint32_t(bytes[off + 1]) << 8;
+    }
+    pk[i] = uint16_t(v);
+  }
+}
+
+__global__ void packets_to_stripes_kernel(const uint16_t *pk, int64_t P, int64_t k, int w,
+                                          uint8_t *bytes, int64_t len) {
+  for (int64_t off = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; off < len;
+       off += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t sym = off / w, sidx = sym / k, j = sym - sidx * k;
+    const uint16_t v = pk[j * P + sidx];
+    bytes[off] = uint8_t(w == 2 && (off & 1) ? (v >> 8) : (v & 0xFF));
+  }
+}
+
+// shard payloads [rows][S * w] <-> packets [rows][P] (lanes >= S are zero)
+__global__ void payload_packets_kernel(const uint8_t *pay, uint16_t *pk, int64_t rows, int64_t S,
+                                       int64_t P, int w, int to_packets, uint8_t *pay_out,
+                                       const uint16_t *pk_in) {
+  const int64_t total = rows * P;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t row = i / P, sidx = i - row * P;
+    if (to_packets) {
+      uint32_t v = 0;
+      if (sidx < S) {
+        const uint8_t *src = pay + (row * S + sidx) * w;
+        v = w == 2 ? uint32_t(src[0]) | (uint32_t(src[1]) << 8) : src[0];
+      }
+      pk[i] = uint16_t(v);
+    } else if (sidx < S) {
+      const uint16_t v = pk_in[i];
+      uint8_t *dst = pay_out + (row * S + sidx) * w;
+      dst[0] = uint8_t(v & 0xFF);
+      if (w == 2) dst[1] = uint8_t(v >> 8);
+    }
+  }
+}
+
+static int grid_for(int64_t total) {
+  return int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
+}
+
+cudaError_t launch_stripes_to_packets(const uint8_t *bytes, int64_t len, int w, int64_t k, int64_t S,
+                                      uint16_t *pk, int64_t P, cudaStream_t s) {
+  stripes_to_packets_kernel<<<grid_for(k * P), 256, 0, s>>>(bytes, len, w, k, S, pk, P);
+  return cudaGetLastError();
+}
+cudaError_t launch_packets_to_stripes(const uint16_t *pk, int64_t P, int64_t k, int w, uint8_t *bytes,
+                                      int64_t len, cudaStream_t s) {
+  packets_to_stripes_kernel<<<grid_for(len), 256, 0, s>>>(pk, P, k, w, bytes, len);
+  return cudaGetLastError();
+}
+cudaError_t launch_payload_packets(const uint8_t *pay, uint16_t *pk, int64_t rows, int64_t S, int64_t P,
+                                   int w, int to_packets, uint8_t *pay_out, const uint16_t *pk_in,
+                                   cudaStream_t s) {
+  payload_packets_kernel<<<grid_for(rows * P), 256, 0, s>>>(pay, pk, rows, S, P, w, to_packets, pay_out,
+                                                             pk_in);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_gen_packets(uint64_t seed, uint64_t cw0, int64_t batch, int64_t len,
                                uint32_t mask, uint16_t *out, int64_t npos, int64_t pkt,
                                cudaStream_t s) {

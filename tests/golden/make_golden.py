@@ -310,6 +310,50 @@ def make_r16_anyk() -> None:
         json.dump(res, f, indent=1)
 
 
+def file_bytes(seed: int, size: int) -> bytes:
+    """Seeded file contents (the counter-based generator, one byte per key)."""
+    return bytes(key(seed, 0, j) & 0xFF for j in range(size))
+
+
+def make_shards() -> None:
+    """Shard files written by the reference CLI (cli.py:40-60, shardfile.py),
+    as sha256 per shard file, for r = 8; r = 16 through the same API without
+    files (2^16 shard files per case): stripe packing + BatchCodec.encode +
+    one concatenated digest of all shard payloads in index order."""
+    import tempfile
+    from binfec import cli as ref_cli
+    from binfec import shardfile as ref_sf
+    res = {"r8": [], "r16": []}
+    for size, k in ((0, 128), (1, 128), (1000, 128), (100000, 128), (5000, 16), (3000, 1)):
+        seed = 1404345800 + size + k
+        with tempfile.TemporaryDirectory() as td:
+            src = os.path.join(td, "in.bin")
+            with open(src, "wb") as fh:
+                fh.write(file_bytes(seed, size))
+            outd = os.path.join(td, "shards")
+            assert ref_cli.main(["encode", "--in", src, "--out", outd, "--r", "8", "--k", str(k)]) == 0
+            shards = []
+            for j in range(256):
+                with open(os.path.join(outd, ref_sf.shard_filename(j)), "rb") as fh:
+                    shards.append(hashlib.sha256(fh.read()).hexdigest()[:32])
+        res["r8"].append({"seed": seed, "size": size, "k": k, "shard_sha256_32": shards})
+    ft = tables_for(16)
+    bt = build_basis_tables(ft, 1 << 16)
+    for size, k in ((100000, 1024), (70000, 32768)):
+        seed = 1404345800 + size + k
+        data = file_bytes(seed, size)
+        stripes = ref_sf.bytes_to_stripes(data, k, 16)
+        cw = ref_batch.BatchCodec(ref_rs.CodeParams(16, k), bt).encode(stripes)
+        h = hashlib.sha256()
+        for j in range(1 << 16):
+            h.update(cw[:, j].astype("<u2").tobytes())
+        hdr = ref_sf.ShardHeader(16, k.bit_length() - 1, 7, size, 0x1100B).pack()
+        res["r16"].append({"seed": seed, "size": size, "k": k, "stripes": int(stripes.shape[0]),
+                           "payloads_sha256": h.hexdigest(), "header7_hex": hdr.hex()})
+    with open(os.path.join(HERE, "golden_shards.json"), "w") as fh:
+        json.dump(res, fh, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["r8", "r16"]
     if "r8" in which:
@@ -321,3 +365,6 @@ if __name__ == "__main__":
     if "r16" in which or "r16_anyk" in which:
         make_r16_anyk()
         print("r16_anyk done", flush=True)
+    if "shards" in which or which == ["r8", "r16"]:
+        make_shards()
+        print("shards done", flush=True)

@@ -165,6 +165,11 @@ int lch_decode_host(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride_in,
  * bit-sliced intermediates exceed it are processed in lane chunks. */
 int lch_set_scratch_limit(lch_ctx *ctx, uint64_t bytes);
 
+/* out[i] = a[i] * b[i] in GF(2^r) (the pointwise step of transform.poly_mul,
+ * transform.py:204-205); out may alias a or b. */
+int lch_pointwise_mul(lch_ctx *ctx, const uint16_t *a, const uint16_t *b, uint16_t *out,
+                      int64_t count, void *stream);
+
 /* Shard-file layouts (reference shardfile.py:16-20,109-140).  A file of
  * `len` bytes is stripes [S][k] of r/8-byte little-endian symbols, zero
  * padded (S = ceil(len / (k r/8))); shard j holds symbol j of every stripe.

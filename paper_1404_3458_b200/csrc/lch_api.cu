@@ -1421,6 +1421,16 @@ int lch_gen_packets(lch_ctx *c, uint64_t seed, uint64_t cw0, int64_t batch, int6
                                static_cast<cudaStream_t>(stream)));
 }
 
+int lch_pointwise_mul(lch_ctx *c, const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
+                      void *stream) {
+  if (!c || count < 0 || (count && (!a || !b || !out))) return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (count == 0) return LCH_OK;
+  c->launches++;
+  return cu(launch_pointwise_mul(a, b, out, count, c->d_log, c->d_exp, c->t.m,
+                                 static_cast<cudaStream_t>(stream)));
+}
+
 // ---- shard-file layouts (shardfile.py:109-140) ----------------------------
 
 int lch_stripes_to_packets(lch_ctx *c, const uint8_t *file, int64_t len, int r, int64_t k,

@@ -1300,8 +1300,30 @@ __global__ void payload_packets_kernel(const uint8_t *pay, uint16_t *pk, int64_t
   }
 }
 
+// out[i] = a[i] * b[i] in GF(2^r) via the log/exp tables (transform.py:204-205)
+__global__ void pointwise_mul_kernel(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
+                                     const uint16_t *log, const uint16_t *exp, uint32_t m) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t x = a[i], y = b[i];
+    uint32_t r = 0;
+    if (x && y) {
+      uint32_t e = uint32_t(__ldg(log + x)) + __ldg(log + y);
+      e = e >= m ? e - m : e;
+      r = __ldg(exp + e);
+    }
+    out[i] = uint16_t(r);
+  }
+}
+
 static int grid_for(int64_t total) {
   return int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
+}
+
+cudaError_t launch_pointwise_mul(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
+                                 const uint16_t *log, const uint16_t *exp, uint32_t m, cudaStream_t s) {
+  pointwise_mul_kernel<<<grid_for(count), 256, 0, s>>>(a, b, out, count, log, exp, m);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stripes_to_packets(const uint8_t *bytes, int64_t len, int w, int64_t k, int64_t S,

@@ -137,13 +137,12 @@ def poly_mul(bt: BasisTables, a: CoeffVec, b: CoeffVec) -> CoeffVec:
     if h2 > bt.max_h:
         raise ValueError(f"product size {h2} exceeds table capacity {bt.max_h}")
     _lib.require_cuda()
-    torch = _lib.torch_mod()
+    # both operands zero-extended to 2h, forward, pointwise product, inverse:
+    # all on the device, one copy in and one out
     dev = _lib.to_device_u16([list(a.data) + [0] * h, list(b.data) + [0] * h])
     run_transform(bt, dev, 0, False)
-    ea, eb = _lib.to_host_u16(dev)
-    mul = bt.ft.mul
-    prod = [mul(int(x), int(y)) for x, y in zip(ea, eb)]
-    pd = _lib.to_device_u16(prod).view(1, h2)
+    _lib.check(_lib.lib.lch_pointwise_mul(bt.ctx.handle, dev[0].data_ptr(), dev[1].data_ptr(),
+                                          dev[0].data_ptr(), h2, _lib.stream_ptr()), "poly_mul")
+    pd = dev[0:1]
     run_transform(bt, pd, 0, True)
-    del torch
     return CoeffVec([int(x) for x in _lib.to_host_u16(pd)[0]])

@@ -333,3 +333,19 @@ def test_decode_per_codeword_r16_vs_oracle(lch, bt16, orc16):
     jh, mh = host(junk), emask[:3].cpu().numpy().astype(np.uint8)
     for r in range(3):
         np.testing.assert_array_equal(host(jout)[r], orc16.decode(k, jh[r], mh[r]), err_msg=f"row {r}")
+
+
+@pytest.mark.parametrize("r,h", [(8, 1), (8, 16), (8, 128), (16, 1024), (16, 1 << 15)])
+def test_poly_mul_vs_oracle(lch, bt8, bt16, orc8, orc16, r, h):
+    """transform.poly_mul (transform.py:189-206): forward of both zero-extended
+    operands, pointwise product, inverse -- all on the GPU."""
+    bt, orc = (bt8, orc8) if r == 8 else (bt16, orc16)
+    a = O.gen_symbols(31, r, 0, 1, h)[0]
+    b = O.gen_symbols(32, r, 0, 1, h)[0]
+    got = lch.poly_mul(bt, lch.CoeffVec([int(x) for x in a]), lch.CoeffVec([int(x) for x in b])).data
+    ea = orc.forward(np.concatenate([a, np.zeros(h, np.uint16)]), 0)
+    eb = orc.forward(np.concatenate([b, np.zeros(h, np.uint16)]), 0)
+    prod = np.array([orc.mul(int(x), int(y)) for x, y in zip(ea, eb)], np.uint16)
+    np.testing.assert_array_equal(np.asarray(got, np.uint16), orc.inverse(prod, 0))
+    if h == 1:
+        assert lch.poly_mul(bt, lch.CoeffVec([1]), lch.CoeffVec([1])).data == [1, 0]  # test_transform.py:137-141

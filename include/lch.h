@@ -161,6 +161,13 @@ int lch_decode_host(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride_in,
                     int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len,
                     int64_t chunk, void *stream);
 
+/* Host helper of the decode pipeline: row r of host_out = the survivors
+ * (bit j of host_bits clear) of row r of host_rx, in order (multi-threaded,
+ * AVX-512 VBMI2 compress-store when available).  No device involved. */
+int lch_compact_rows(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride,
+                     const uint32_t *host_bits, int64_t n, int64_t rows, uint16_t *host_out,
+                     int64_t out_stride);
+
 /* Device scratch budget per call (bytes, default 4 GiB): batches whose
  * bit-sliced intermediates exceed it are processed in lane chunks. */
 int lch_set_scratch_limit(lch_ctx *ctx, uint64_t bytes);

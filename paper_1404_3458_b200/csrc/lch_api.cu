@@ -2,15 +2,19 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
+#include <thread>
 #include <mutex>
 #include <type_traits>
 #include <utility>
 #include <vector>
 
 #include "../../include/lch.h"
+#include "lch_host.h"
 #include "lch_kernels.h"
 #include "lch_tables.h"
 
@@ -29,6 +33,10 @@ struct lch_ctx {
   size_t scratch_limit = size_t(4) << 30;
   std::vector<std::pair<int64_t, uint16_t *>> enc_tabs;  // encode-by-decode tables per k
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;         // host-buffer pipeline copy streams
+  std::vector<std::pair<size_t, void *>> pinned;          // page-locked staging slots
+  std::unique_ptr<HostPool> pool;                          // host workers (survivor compaction)
+  cudaEvent_t ring_ev[16] = {};                            // upload_small ring slots
+  size_t ring_next = 0;
   std::mutex mu;
 };
 
@@ -510,6 +518,10 @@ void lch_destroy(lch_ctx *c) {
     for (auto &e : c->enc_tabs) cudaFree(e.second);
     if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
     if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+    for (auto &e : c->pinned)
+      if (e.second) cudaFreeHost(e.second);
+    for (cudaEvent_t e : c->ring_ev)
+      if (e) cudaEventDestroy(e);
   }
   delete c;
 }
@@ -1230,7 +1242,59 @@ struct HostArray {
   uint8_t *dst = nullptr;        // host output (or null)
   size_t row_bytes = 0;          // bytes copied per row
   size_t pitch = 0;              // host bytes between rows
+  // optional host stage: fills rows [r0, r0 + nr) into a page-locked staging
+  // buffer (row_bytes per row) that is then copied instead of src
+  std::function<void(int64_t r0, int64_t nr, uint8_t *staging)> prep;
 };
+
+// grow-only page-locked staging buffers of the context
+uint8_t *pinned_buffer(lch_ctx *c, size_t idx, size_t bytes) {
+  std::lock_guard<std::mutex> g(c->mu);
+  if (c->pinned.size() <= idx) c->pinned.resize(idx + 1, {0, nullptr});
+  auto &e = c->pinned[idx];
+  if (e.first < bytes) {
+    if (e.second) cudaFreeHost(e.second);
+    e.second = nullptr;
+    e.first = 0;
+    if (cudaHostAlloc(&e.second, bytes, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    e.first = bytes;
+  }
+  return static_cast<uint8_t *>(e.second);
+}
+
+// Small host -> device uploads through a ring of page-locked slots: an
+// asynchronous copy from pageable memory would serialise the stream with
+// the host (and with work queued before the call).
+int upload_small(lch_ctx *c, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  constexpr size_t SLOT = size_t(1) << 20;
+  if (bytes > SLOT) return cu(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  size_t slot;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    slot = c->ring_next++ % 16;
+  }
+  uint8_t *ring = pinned_buffer(c, 1000, 16 * SLOT);  // one allocation for all slots
+  if (!ring) return LCH_ENOMEM;
+  uint8_t *stg = ring + slot * SLOT;
+  cudaEvent_t &ev = c->ring_ev[slot];
+  if (ev) LCH_TRY(cu(cudaEventSynchronize(ev)));
+  else LCH_TRY(cu(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)));
+  std::memcpy(stg, src, bytes);
+  LCH_TRY(cu(cudaMemcpyAsync(dst, stg, bytes, cudaMemcpyHostToDevice, s)));
+  return cu(cudaEventRecord(ev, s));
+}
+
+HostPool &host_pool(lch_ctx *c) {
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->pool) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    c->pool.reset(new HostPool(int(std::max(1u, std::min(hc ? hc : 1u, 16u) - 1))));
+  }
+  return *c->pool;
+}
 
 int host_streams(lch_ctx *c) {
   std::lock_guard<std::mutex> g(c->mu);
@@ -1245,7 +1309,7 @@ using ChunkFn = std::function<int(const std::vector<const uint8_t *> &, uint8_t 
 
 int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
                   const std::vector<HostArray> &ins, const HostArray &out, const ChunkFn &compute) {
-  constexpr int NS = 3;
+  constexpr int NS = 4;
   LCH_TRY(host_streams(c));
   const int ni = int(ins.size());
   std::vector<cudaEvent_t> evs;
@@ -1277,27 +1341,64 @@ int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
   LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, entry, 0)));
   LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, entry, 0)));
   const int64_t nchunks = (rows + chunk - 1) / chunk;
+  // LCH_PIPE_TRACE=1: per-chunk stage timestamps on stderr (diagnostics)
+  static const bool trace = std::getenv("LCH_PIPE_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  mark(s);
   for (int64_t i = 0; i < nchunks; ++i) {
     const int k = int(i % NS);
     const int64_t r0 = i * chunk, nr = std::min(chunk, rows - r0);
-    if (i >= NS) LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, ev_free[k], 0)));
+    // input slot k is reusable once the codec of chunk i - NS has consumed it
+    if (i >= NS) LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, ev_done[k], 0)));
     std::vector<const uint8_t *> dptr(static_cast<size_t>(ni), nullptr);
     for (int a = 0; a < ni; ++a) {
       const HostArray &h = ins[a];
       uint8_t *d = din[size_t(k) * ni + a];
-      LCH_TRY(cu(cudaMemcpy2DAsync(d, h.row_bytes, h.src + size_t(r0) * h.pitch, h.pitch, h.row_bytes,
-                                   size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
+      if (h.prep) {
+        // the staging slot is free once the H2D copy of chunk i - NS has run
+        uint8_t *stg = pinned_buffer(c, size_t(k) * ni + a, h.row_bytes * size_t(chunk));
+        if (!stg) return LCH_ENOMEM;
+        if (i >= NS) LCH_TRY(cu(cudaEventSynchronize(ev_in[k])));
+        h.prep(r0, nr, stg);
+        LCH_TRY(cu(cudaMemcpyAsync(d, stg, h.row_bytes * size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
+      } else {
+        LCH_TRY(cu(cudaMemcpy2DAsync(d, h.row_bytes, h.src + size_t(r0) * h.pitch, h.pitch, h.row_bytes,
+                                     size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
+      }
       dptr[size_t(a)] = d;
     }
+    mark(c->s_h2d);
     LCH_TRY(cu(cudaEventRecord(ev_in[k], c->s_h2d)));
     LCH_TRY(cu(cudaStreamWaitEvent(s, ev_in[k], 0)));
+    // output slot k is reusable once the D2H copy of chunk i - NS has run
+    if (i >= NS) LCH_TRY(cu(cudaStreamWaitEvent(s, ev_free[k], 0)));
     const int crc = compute(dptr, dout[k], r0, nr);
     if (crc != LCH_OK) return crc;
+    mark(s);
     LCH_TRY(cu(cudaEventRecord(ev_done[k], s)));
     LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, ev_done[k], 0)));
     LCH_TRY(cu(cudaMemcpy2DAsync(out.dst + size_t(r0) * out.pitch, out.pitch, dout[k], out.row_bytes,
                                  out.row_bytes, size_t(nr), cudaMemcpyDeviceToHost, c->s_d2h)));
+    mark(c->s_d2h);
     LCH_TRY(cu(cudaEventRecord(ev_free[k], c->s_d2h)));
+  }
+  if (trace) {
+    cudaDeviceSynchronize();
+    std::fprintf(stderr, "pipeline %lld chunks:", (long long)nchunks);
+    for (size_t i = 1; i < tev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      std::fprintf(stderr, " %s%.2f", (i - 1) % 3 == 0 ? "| h2d " : (i - 1) % 3 == 1 ? "cmp " : "d2h ", ms);
+    }
+    std::fprintf(stderr, "\n");
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
   for (int64_t i = std::max<int64_t>(0, nchunks - NS); i < nchunks; ++i)
     LCH_TRY(cu(cudaStreamWaitEvent(s, ev_free[i % NS], 0)));
@@ -1369,11 +1470,48 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
   uint32_t *d_shared = nullptr;
   if (shared) {
     LCH_TRY(sc.alloc(d_shared, size_t(words)));
-    LCH_TRY(cu(cudaMemcpyAsync(d_shared, host_bits, size_t(words) * 4, cudaMemcpyHostToDevice, s)));
+    LCH_TRY(upload_small(c, d_shared, host_bits, size_t(words) * 4, s));
   }
   const size_t in_row = size_t(n * lanes_per_row) * 2, out_row = size_t(k * lanes_per_row) * 2;
   if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / in_row));
   chunk = std::min(chunk, rows);
+  if (shared && !pkt && n >= 32 && !std::getenv("LCH_NO_COMPACT")) {
+    // Only the survivors cross PCIe: the host compacts each row (AVX-512
+    // compress-store on the worker pool) into page-locked staging, the
+    // device expands the rows back (erased positions read as zero; the
+    // decoder ignores them, rs.py:130-134).
+    const int64_t surv = n - counts[0];
+    std::vector<int32_t> rank(static_cast<size_t>(n), -1);
+    for (int64_t j = 0, r = 0; j < n; ++j)
+      if (!((host_bits[j >> 5] >> (j & 31)) & 1u)) rank[size_t(j)] = int32_t(r++);
+    int32_t *d_rank = nullptr;
+    LCH_TRY(sc.alloc(d_rank, size_t(n)));
+    LCH_TRY(upload_small(c, d_rank, rank.data(), size_t(n) * 4, s));
+    HostPool &pool = host_pool(c);
+    const size_t crow = size_t(std::max<int64_t>(surv, 1)) * 2;
+    if (chunk == 0 || chunk > rows) chunk = std::min(rows, std::max<int64_t>(1, int64_t((size_t(64) << 20) / (size_t(n) * 2))));
+    std::vector<HostArray> cins(1);
+    cins[0].row_bytes = crow;
+    cins[0].prep = [&](int64_t r0, int64_t nr, uint8_t *stg) {
+      compact_rows(pool, host_rx + r0 * stride_in, stride_in, host_bits, n, nr,
+                   reinterpret_cast<uint16_t *>(stg), std::max<int64_t>(surv, 1));
+    };
+    HostArray cout;
+    cout.dst = reinterpret_cast<uint8_t *>(host_out);
+    cout.row_bytes = size_t(k) * 2;
+    cout.pitch = size_t(stride_out) * 2;
+    return host_pipeline(c, s, rows, chunk, cins, cout,
+                         [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr) {
+                           Scratch cs(s);
+                           uint16_t *full = nullptr;
+                           LCH_TRY(cs.alloc(full, size_t(nr) * size_t(n)));
+                           LCH_TRY(cu(launch_expand_rows(reinterpret_cast<const uint16_t *>(d[0]),
+                                                         std::max<int64_t>(surv, 1), d_rank, full, n, nr, s)));
+                           c->launches++;
+                           return decode_any(c, full, n, d_shared, 1, reinterpret_cast<uint16_t *>(o), k, nr,
+                                             k, 0, counts.data(), stream);
+                         });
+  }
   std::vector<HostArray> ins(shared ? 1 : 2);
   ins[0].src = reinterpret_cast<const uint8_t *>(host_rx);
   ins[0].row_bytes = in_row;
@@ -1393,6 +1531,13 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
                                            reinterpret_cast<uint16_t *>(o), k, nr * lanes_per_row, k, pkt,
                                            counts.data() + (shared ? 0 : r0), stream);
                        });
+}
+
+int lch_compact_rows(lch_ctx *c, const uint16_t *host_rx, int64_t stride, const uint32_t *host_bits,
+                     int64_t n, int64_t rows, uint16_t *host_out, int64_t out_stride) {
+  if (!c || !host_rx || !host_bits || !host_out || n < 0 || rows < 0 || stride < n) return LCH_EINVAL;
+  compact_rows(host_pool(c), host_rx, stride, host_bits, n, rows, host_out, out_stride);
+  return LCH_OK;
 }
 
 int lch_set_scratch_limit(lch_ctx *c, uint64_t bytes) {

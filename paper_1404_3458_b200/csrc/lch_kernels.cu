@@ -1320,6 +1320,23 @@ static int grid_for(int64_t total) {
   return int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
 }
 
+__global__ void expand_rows_kernel(const uint16_t *comp, int64_t cs, const int32_t *rank, uint16_t *full,
+                                   int64_t n, int64_t rows) {
+  const int64_t total = rows * n;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / n, j = i - r * n;
+    const int32_t q = __ldg(rank + j);
+    full[i] = q >= 0 ? comp[r * cs + q] : uint16_t(0);
+  }
+}
+
+cudaError_t launch_expand_rows(const uint16_t *comp, int64_t comp_stride, const int32_t *rank, uint16_t *full,
+                               int64_t n, int64_t rows, cudaStream_t s) {
+  expand_rows_kernel<<<grid_for(rows * n), 256, 0, s>>>(comp, comp_stride, rank, full, n, rows);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pointwise_mul(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
                                  const uint16_t *log, const uint16_t *exp, uint32_t m, cudaStream_t s) {
   pointwise_mul_kernel<<<grid_for(count), 256, 0, s>>>(a, b, out, count, log, exp, m);

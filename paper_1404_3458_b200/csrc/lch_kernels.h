@@ -174,6 +174,9 @@ cudaError_t launch_decode_rows(const uint16_t *logs, const uint32_t *bits, const
 cudaError_t launch_xor_views(uint16_t *out, int64_t so, const uint16_t *a, int64_t sa,
                              const uint16_t *b, int64_t sb, int64_t batch, int64_t len, int64_t pkt,
                              cudaStream_t s);
+// full[r][j] = rank[j] >= 0 ? comp[r][rank[j]] : 0 (survivor rows -> n-wide rows)
+cudaError_t launch_expand_rows(const uint16_t *comp, int64_t comp_stride, const int32_t *rank, uint16_t *full,
+                               int64_t n, int64_t rows, cudaStream_t s);
 cudaError_t launch_pointwise_mul(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
                                  const uint16_t *log, const uint16_t *exp, uint32_t m, cudaStream_t s);
 cudaError_t launch_stripes_to_packets(const uint8_t *bytes, int64_t len, int w, int64_t k, int64_t S,

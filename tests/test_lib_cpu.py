@@ -192,3 +192,22 @@ def test_host_pipeline_too_many_from_host_counts():
         assert rc == _lib.LCH_ECUDA
     with pytest.raises(Exception):
         lch.BatchCodec(lch.CodeParams(8, 128), bt).decode(rx, set(range(129)))
+
+
+def test_host_compaction_of_survivors():
+    """lch_compact_rows (host side of the decode pipeline): survivors in order,
+    vector and scalar paths (n multiple of 32 or not)."""
+    ft = lch.tables_for(8)
+    bt = lch.build_basis_tables(ft, 256)
+    rng = np.random.default_rng(4)
+    for n in (256, 96, 40):
+        rows = 37
+        rx = rng.integers(0, 65536, (rows, n + 3)).astype(np.uint16)  # stride n + 3
+        mask = rng.random(n) < 0.45
+        bits = _lib.bitmask_from_positions(n, np.nonzero(mask)[0])
+        surv = int((~mask).sum())
+        out = np.zeros((rows, surv + 1), np.uint16)
+        rc = _lib.lib.lch_compact_rows(bt.ctx.handle, rx.ctypes.data, n + 3, bits.ctypes.data, n, rows,
+                                       out.ctypes.data, surv + 1)
+        assert rc == _lib.LCH_OK
+        np.testing.assert_array_equal(out[:, :surv], rx[:, :n][:, ~mask])

@@ -470,14 +470,14 @@ struct FactorLoader {
   uint32_t v[PER];
   int slot[PER];
   __device__ __forceinline__ void fetch(const PassParams &p, const uint32_t *tpos, uint32_t base) {
-    const int half = 1 << (p.tpb - 1 < 0 ? 0 : p.tpb - 1);
-    const int n = p.nops * half;
+    const int lh = p.tpb - 1 < 0 ? 0 : p.tpb - 1;  // log2 of the pairs per op
+    const int n = p.nops << lh;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int e = threadIdx.x + k * NT;
       slot[k] = -1;
       if (p.tpb > 0 && e < n) {
-        const int o = e / half, pp = e - o * half;
+        const int o = e >> lh, pp = e & ((1 << lh) - 1);
         const PassOp &op = p.ops[o];
         const int m = op.mloc;
         const int qu = ((pp >> m) << (m + 1)) | (pp & ((1 << m) - 1));

@@ -51,7 +51,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1404_3458_b200.dist import env_rank  # noqa: E402
+from paper_1404_3458_b200.dist import env_rank, max_over_ranks  # noqa: E402
+
+# NCCL for the driver's multi-GPU runs; LCH_DIST_BACKEND=gloo runs the same
+# multi-rank logic (CPU collectives) e.g. with several ranks on one device.
+DIST_BACKEND = os.environ.get("LCH_DIST_BACKEND", "nccl")
+
+
+def dist_device():
+    return "cuda" if DIST_BACKEND == "nccl" else "cpu"
 
 R_BITS, N, K = 16, 1 << 16, 1 << 15
 BATCH = 4096
@@ -315,9 +323,7 @@ class Timer:
         step_ms = t0.elapsed_time(t1) / steps
         ph = [float(np.mean([m[i].elapsed_time(m[i + 1]) for m in marks])) for i in range(len(phases))]
         if world > 1:
-            t = torch.tensor([step_ms] + ph, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            vals = [float(x) for x in t.tolist()]
+            vals = max_over_ranks([step_ms] + ph, dist_device())
             step_ms, ph = vals[0], vals[1:]
         return step_ms, dict(zip([n for n, _ in phases], ph)), int(launches), clk.summary()
 
@@ -465,9 +471,7 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / e2e_steps
         if world > 1:
-            t = torch.tensor([e2e_ms], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+            e2e_ms = max_over_ranks([e2e_ms], dist_device())[0]
         assert torch.equal(h_out, h_msg), "e2e round trip failed"
         assert torch.equal(h_par, parity.cpu()), "e2e parity differs from the device path"
         surv = N - int(np.unpackbits(h_bits.view(np.uint8)).sum())
@@ -722,9 +726,13 @@ def main():
     import torch.distributed as dist
 
     rank, world, local = env_rank()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if DIST_BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(DIST_BACKEND)
     import paper_1404_3458_b200 as lch
     from paper_1404_3458_b200 import _lib
 

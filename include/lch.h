@@ -138,7 +138,7 @@ int lch_encode_k(lch_ctx *ctx, const uint16_t *msg, int64_t stride_in, uint16_t 
 /* General-k erasure decode (rs.decode, rs.py:99-149 with the power-of-two
  * restriction of rs.py:43-44 lifted): recovers positions [0, k) from any
  * <= n - k erasures.  Row layout: shared = 1 (one pattern) or 0 (one per
- * row; k <= n/2).  Packet layout: shared = 1 (one pattern) or 0 (one pattern
+ * row).  Packet layout: shared = 1 (one pattern) or 0 (one pattern
  * per stripe group, erasure_bits [batch / packet_len][2^r / 32]). */
 int lch_decode_k(lch_ctx *ctx, const uint16_t *rx, int64_t stride_in,
                  const uint32_t *erasure_bits, int shared, uint16_t *out, int64_t stride_out,

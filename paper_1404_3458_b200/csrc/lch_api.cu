@@ -993,7 +993,7 @@ static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in
   const int64_t n = int64_t(c->t.order);
   const int lgo = std::max(ceil_lg(k), 1);
   const int64_t kf = int64_t(1) << lgo;  // forward length (first kf outputs)
-  if (lgo > r - 1) return LCH_EUNSUPPORTED;
+  const bool folded = lgo <= r - 1;      // k > n/2: the unfolded schedule (see erasure_core)
   return dispatch(c, [&](auto RC, auto PC) -> int {
     constexpr int R = decltype(RC)::value;
     constexpr uint32_t P = decltype(PC)::value;
@@ -1030,16 +1030,18 @@ static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in
       const int64_t nb = std::min(ch, batch - b0);
       RawIO in_io = shift_io(in0, b0), out_io = shift_io(out0, b0);
       std::vector<LOp> a;
-      for (int i = 0; i + 1 < r; ++i) a.push_back({OP_INV, i, 0u, nullptr});
-      a.push_back({OP_SCALE, 0, 0, c->d_b_lo});
+      const int ninv = folded ? r - 1 : r;
+      for (int i = 0; i < ninv; ++i) a.push_back({OP_INV, i, 0u, nullptr});
+      a.push_back({OP_SCALE, 0, 0, folded ? c->d_b_lo : c->d_b_prod});
       auto plan_a = plan_passes(a, r, true, false);
       LCH_TRY((run_plan<R, P>(c, plan_a, r, nb, &in_io, nullptr, nullptr, x, s, t1, lgo)));
       std::vector<int> rest;
       const auto &lb = plan_a.back().bits;
-      for (int b = 0; b + 1 < r; ++b)
+      for (int b = 0; b < ninv; ++b)
         if (std::find(lb.begin(), lb.end(), b) == lb.end()) rest.push_back(b);
-      rest.push_back(r - 1);
-      LCH_TRY((run_gather<R, P>(c, x, t, r, lgo, nb, rest, r - 1, c->t.w_prime[r - 1], t1, s)));
+      if (folded) rest.push_back(r - 1);
+      LCH_TRY((run_gather<R, P>(c, x, t, r, lgo, nb, rest, folded ? r - 1 : -1,
+                                folded ? c->t.w_prime[r - 1] : 0u, t1, s)));
       std::vector<LOp> b = {{OP_SCALE, 0, 0, c->d_b_prod_inv}};
       for (int i = lgo - 1; i >= 0; --i) b.push_back({OP_FWD, i, 0u, nullptr});
       LCH_TRY((run_plan<R, P>(c, plan_passes(b, lgo, false, true), lgo, nb, nullptr, t, &out_io, t, s)));

@@ -282,3 +282,23 @@ def test_general_encoder_equals_encode_by_decode(lch, bt8, bt16, r, k, B):
     if r == 16:
         m0 = host(msg)[0]
         np.testing.assert_array_equal(outs[0][0], O.Oracle(16).encode_any(k, m0)[k:])
+
+
+@pytest.mark.parametrize("k", [192, 240])
+def test_row_per_codeword_general_k_above_half(lch, bt8, orc8, k):
+    """Per-row patterns with k > n/2 (unfolded decode schedule), B >= 1024 so the
+    bit-sliced path runs."""
+    import torch
+    from paper_1404_3458_b200 import _lib
+    n, B = 256, 1100
+    msg = O.gen_symbols(SEED + 3 * k, 8, 0, B, k)
+    cw = np.concatenate([msg, orc8.encode_any_batch(k, msg, nthreads=8)], axis=1)
+    masks = O.gen_erasures(SEED + 5, n, n - k, 0, B).astype(bool)
+    junk = O.gen_symbols(SEED + 6, 8, 0, B, n)
+    for rx, want in ((np.where(masks, 0x33, cw).astype(np.uint16), msg),
+                     (junk, orc8.decode_any_batch(k, junk, masks.astype(np.uint8), nthreads=8))):
+        out = torch.empty((B, k), dtype=torch.int16, device="cuda")
+        bits = bits_of(masks)
+        _lib.check(_lib.lib.lch_decode_k(bt8.ctx.handle, dev(rx).data_ptr(), n, bits.data_ptr(), 0,
+                                         out.data_ptr(), k, B, k, 0, None, _lib.stream_ptr()))
+        np.testing.assert_array_equal(host(out), want)

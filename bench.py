@@ -554,6 +554,46 @@ def run_stripe(args, torch, lch, _lib, world, rank, local):
                              peak, peak_src),
         "e2e": None,
     })
+    if not args.no_e2e:
+        # host-buffer API (lch_encode_host / lch_decode_host, packet layout) on a
+        # pinned subset of the stripe groups (pinning 32 GiB would dominate the run)
+        import torch.distributed as dist
+        import ctypes as C
+        Ge = min(G, 8)
+        h_cw = cw[:Ge].cpu().pin_memory()
+        h_out = torch.empty((Ge, k, PKT), dtype=torch.int16, pin_memory=True)
+        h_bits = bits[:Ge].cpu().numpy().view(np.uint32).copy()
+        h_par = torch.empty((Ge, N - k, PKT), dtype=torch.int16, pin_memory=True)
+        le = Ge * PKT
+
+        def e2e_step():
+            _lib.check(_lib.lib.lch_encode_host(ctx, h_cw.data_ptr(), N, h_par.data_ptr(), N - k, le, k, PKT, 0,
+                                                s))
+            _lib.check(_lib.lib.lch_decode_host(ctx, h_cw.data_ptr(), N, h_bits.ctypes.data, 0, h_out.data_ptr(),
+                                                k, le, k, PKT, 0, s))
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tm = Timer(torch, stream)
+        a, b = tm.ev(), tm.ev()
+        a.record(stream)
+        for _ in range(2):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b) / 2
+        if world > 1:
+            e2e_ms = max_over_ranks([e2e_ms], dist_device())[0]
+        assert torch.equal(h_out, h_cw[:, :k]), "stripe e2e round trip failed"
+        assert torch.equal(h_par, h_cw[:, k:]), "stripe e2e parity differs"
+        res["e2e"] = {"value": round(world * 2 * le * k * 2 / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                      "h2d_bytes_per_step": le * k * 2 + le * N * 2,
+                      "d2h_bytes_per_step": le * (N - k) * 2 + le * k * 2,
+                      "ms_per_step": round(e2e_ms, 3),
+                      "sample": f"{Ge} stripe groups per GPU ({Ge * PKT * k * 2 / 2**30:.2f} GiB of message), "
+                                "pinned host buffers"}
     if rank == 0 and not args.no_cpu:
         nth = cpu_threads()
         res["cpu_baseline"] = cpu_stripe(k, max(8, min(nth, 64)), nth)

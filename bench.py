@@ -483,7 +483,7 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
                              "H2D / kernel / D2H overlap on three streams; the received words' "
                              "survivors are compacted on the host so erased symbols, which the "
                              "decoder ignores, do not cross PCIe)"}
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         nth = cpu_threads()
         res["cpu_baseline"] = cpu_codec(max(8, min(nth, 64)), nth)
     return res
@@ -594,7 +594,7 @@ def run_stripe(args, torch, lch, _lib, world, rank, local):
                       "ms_per_step": round(e2e_ms, 3),
                       "sample": f"{Ge} stripe groups per GPU ({Ge * PKT * k * 2 / 2**30:.2f} GiB of message), "
                                 "pinned host buffers"}
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         nth = cpu_threads()
         res["cpu_baseline"] = cpu_stripe(k, max(8, min(nth, 64)), nth)
     return res
@@ -634,7 +634,7 @@ def run_transform_wl(args, torch, lch, _lib, world, rank, local):
     res.update({f"{k}_gbs": round(world * per / (v * 1e-3) / 1e9, 2) for k, v in ph.items()})
     res["roofline"] = roofline("forward transform (4 passes)", per, ph["forward"], peak, peak_src)
     res["e2e"] = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_transform(max(8, cpu_threads()), cpu_threads())
     return res
 
@@ -676,7 +676,7 @@ def run_pcw(args, torch, lch, _lib, world, rank, local):
     res["roofline"] = roofline("decode pipeline (algorithmic: survivors + output + bitmask)", alg,
                                ph["decode"], peak, peak_src)
     res["e2e"] = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_pcw(max(8, min(cpu_threads(), 32)), cpu_threads())
     return res
 
@@ -740,7 +740,7 @@ def run_r8(args, torch, lch, _lib, world, rank, local):
     res.update({"encode_ms": round(ph["encode"], 4), "decode_ms": round(ph["decode"], 4)})
     res["roofline"] = roofline("encode (latency bound)", 2 * n * B, ph["encode"], peak, peak_src)
     res["e2e"] = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_r8(cpu_threads())
     return res
 

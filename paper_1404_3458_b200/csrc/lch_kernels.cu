@@ -10,6 +10,7 @@
 // in registers) or the bit-sliced intermediate buffer (straight 2 KB block
 // copies, laid out exactly like the shared-memory tile).
 #include <algorithm>
+#include <atomic>
 
 #include "lch_device.cuh"
 #include "lch_kernels.h"
@@ -1049,14 +1050,34 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
   }
 }
 
-cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(locator16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         65536 * 2);
-    if (e != cudaSuccess) return e;
-    attr = true;
+// The dynamic shared-memory opt-in is a per-device function attribute: set it
+// once per (kernel, device) — a process may drive several GPUs.
+template <class K>
+static cudaError_t smem_optin(K *kernel, int bytes, std::atomic<uint64_t> &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+static int sm_count() {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) {
+    cudaGetLastError();
+    nsm = 148;
   }
+  return nsm;
+}
+
+cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s) {
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = smem_optin(locator16_kernel, 65536 * 2, done);
+  if (e != cudaSuccess) return e;
   locator16_kernel<<<unsigned(p.nvec), LOC_NT, 65536 * 2, s>>>(p);
   return cudaGetLastError();
 }
@@ -1154,21 +1175,10 @@ template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   const bool raw = p.in_mode == IO_RAW || p.out_mode == IO_RAW;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(pass_kernel<R, POLY>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(pass_smem_bytes(R, TPB_MAX, true)));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = smem_optin(pass_kernel<R, POLY>, int(pass_smem_bytes(R, TPB_MAX, true)), done);
+  if (e != cudaSuccess) return e;
+  const int nsm = sm_count();
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
   const int64_t ctas = std::min<int64_t>(total, int64_t(2) * nsm);
   pass_kernel<R, POLY><<<unsigned(ctas), NT, smem, s>>>(p);
@@ -1179,14 +1189,9 @@ template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s) {
   const size_t smem = gather_smem_bytes(R, p);
   if (smem > GATHER_SMEM_MAX) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gather_kernel<R, POLY>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(GATHER_SMEM_MAX));
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = smem_optin(gather_kernel<R, POLY>, int(GATHER_SMEM_MAX), done);
+  if (e != cudaSuccess) return e;
   dim3 grid(1u << (p.lgH_in - p.nbits), unsigned(ngroups) * (32u >> p.lwpc));
   gather_kernel<R, POLY><<<grid, GNT, smem, s>>>(p);
   return cudaGetLastError();

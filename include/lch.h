@@ -27,6 +27,9 @@
  *    ZeroDivisionError (field.py:83-84).
  *  - There is no CPU fallback: without a CUDA device every compute entry point
  *    returns LCH_ECUDA.
+ *  - A context uploads its tables to the device current at its first compute
+ *    call and stays bound to it (calls with another current device return
+ *    LCH_EINVAL); use one context per GPU.
  */
 #ifndef LCH_H
 #define LCH_H

@@ -59,7 +59,12 @@ int upload(T *&dst, const std::vector<T> &src) {
 
 int ensure_device(lch_ctx *c) {
   std::lock_guard<std::mutex> g(c->mu);
-  if (c->dev_ready) return LCH_OK;
+  if (c->dev_ready) {
+    // a context's tables live on the device that was current at first use
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return LCH_ECUDA;
+    return cur == c->device ? LCH_OK : LCH_EINVAL;
+  }
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
     cudaGetLastError();

@@ -673,30 +673,27 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         }
         if (has_next && !(p.dbg & 64)) nfl.put(fac[fb ^ 1]);
       } else if (last_reg) {
-        // Drain the tile through the staging half-buffer with bulk stores
-        // (asynchronous: they overlap the next tile's rounds).
-        uint4 *stg = smem + stage_offset_u4<R>();
+        // Drain the tile with bulk stores through a private 4 KB staging area
+        // per warp (two positions at a time): only warp-level syncs, and the
+        // stores overlap the next tile's rounds.
+        uint4 *stg = smem + stage_offset_u4<R>() + warp * 2 * U4;
         uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
-        const int HALF = TP >> 1;
+        if (active) {
+          const int qs[4] = {q0, q0 | M0, q0 | M1, q0 | M0 | M1};
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (lane == 0) tma_store_wait_read();
-          __syncthreads();
-          if (active) {
-            const int qs[4] = {q0, q0 | M0, q0 | M1, q0 | M0 | M1};
-            if ((qs[0] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[0] & (HALF - 1)) * U4, lane, a0);
-            if ((qs[1] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[1] & (HALF - 1)) * U4, lane, a1);
-            if (has1) {
-              if ((qs[2] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[2] & (HALF - 1)) * U4, lane, a2);
-              if ((qs[3] >= HALF) == (h == 1)) Blk<R>::store(stg + (qs[3] & (HALF - 1)) * U4, lane, a3);
+          for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !has1) break;
+            if (lane == 0) tma_store_wait_read();  // this warp's previous bulk stores read their data
+            __syncwarp();
+            Blk<R>::store(stg, lane, h ? a2 : a0);
+            Blk<R>::store(stg + U4, lane, h ? a3 : a1);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0 && !(p.dbg & 5)) {
+              tma_store_1d(dst + size_t(base | tpos[qs[2 * h]]) * U4, stg, U4 * 16);
+              tma_store_1d(dst + size_t(base | tpos[qs[2 * h + 1]]) * U4, stg + U4, U4 * 16);
+              tma_store_commit();
             }
-          }
-          fence_proxy_async();
-          __syncthreads();
-          if (lane == 0 && !(p.dbg & 5)) {
-            for (int q = warp; q < HALF; q += NWARP)
-              tma_store_1d(dst + size_t(base | tpos[h * HALF + q]) * U4, stg + q * U4, U4 * 16);
-            tma_store_commit();
           }
         }
         if (has_next && !(p.dbg & 64)) nfl.put(fac[fb ^ 1]);

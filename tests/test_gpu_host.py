@@ -138,3 +138,24 @@ def test_packet_host_pipeline(lch, bt8):
                                         hout.data_ptr(), k, G * P, k, P, 2, _lib.stream_ptr()))
     torch.cuda.synchronize()
     assert torch.equal(hout, hm)
+
+
+@pytest.mark.parametrize("count", [0, 1, 128])
+def test_decode_host_edge_counts(lch, bt8, orc8, count):
+    """Host pipeline with the survivor compaction: empty pattern (copy), a
+    single erasure, and the maximum; a batch that is not a multiple of the chunk."""
+    import torch
+    from paper_1404_3458_b200._lib import bitmask_from_positions
+    from paper_1404_3458_b200.rs import decode_host
+    cp = lch.CodeParams(8, 128)
+    B = 1300
+    msg = O.gen_symbols(41, 8, 0, B, 128)
+    cw = np.concatenate([msg, orc8.encode_batch(128, msg, nthreads=8)], axis=1)
+    erased = np.sort(np.random.default_rng(count).choice(256, count, replace=False))
+    rx = cw.copy()
+    rx[:, erased] = 0xEE
+    hrx = pinned(rx)
+    out = torch.empty((B, 128), dtype=torch.int16, pin_memory=True)
+    decode_host(cp, bt8, hrx, bitmask_from_positions(256, erased), out, 500)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.numpy().view(np.uint16), msg)

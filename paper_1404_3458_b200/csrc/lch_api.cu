@@ -1297,8 +1297,15 @@ int upload_small(lch_ctx *c, void *dst, const void *src, size_t bytes, cudaStrea
 HostPool &host_pool(lch_ctx *c) {
   std::lock_guard<std::mutex> g(c->mu);
   if (!c->pool) {
-    const unsigned hc = std::thread::hardware_concurrency();
-    c->pool.reset(new HostPool(int(std::max(1u, std::min(hc ? hc : 1u, 16u) - 1))));
+    // share the host cores between the ranks of one node (torchrun exports
+    // LOCAL_WORLD_SIZE); LCH_HOST_THREADS overrides
+    unsigned hc = std::thread::hardware_concurrency();
+    if (!hc) hc = 1;
+    const char *lws = std::getenv("LOCAL_WORLD_SIZE");
+    const unsigned ranks = lws ? unsigned(std::max(1, std::atoi(lws))) : 1u;
+    unsigned nt = std::max(1u, std::min(hc / ranks, 16u));
+    if (const char *ov = std::getenv("LCH_HOST_THREADS")) nt = unsigned(std::max(1, std::atoi(ov)));
+    c->pool.reset(new HostPool(int(nt) - 1));
   }
   return *c->pool;
 }

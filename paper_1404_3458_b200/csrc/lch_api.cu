@@ -38,6 +38,7 @@ struct lch_ctx {
   cudaEvent_t ring_ev[16] = {};                            // upload_small ring slots
   size_t ring_next = 0;
   std::mutex mu;
+  std::mutex host_mu;  // serialises the host-buffer entry points (shared staging, pool)
 };
 
 namespace {
@@ -1098,7 +1099,14 @@ static int decode_any(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const u
     c->launches++;
     return LCH_OK;
   }
-  if (!shared && !pkt) return decode_per_codeword(c, rx, stride_in, bits, out, stride_out, batch, k, s);
+  if (!shared && !pkt) {
+    // phi (n symbols) + -log Pi' + the bit-sliced intermediates per codeword
+    const int64_t ch = chunk_lanes(c, batch, 0, size_t(n) * 2 * 4);
+    for (int64_t b0 = 0; b0 < batch; b0 += ch)
+      LCH_TRY(decode_per_codeword(c, rx + b0 * stride_in, stride_in, bits + b0 * words, out + b0 * stride_out,
+                                  stride_out, std::min(ch, batch - b0), k, s));
+    return LCH_OK;
+  }
   const int lgo = std::max(ceil_lg(k), 1);
   const int64_t kf = int64_t(1) << lgo;
   Scratch sc(s);
@@ -1433,6 +1441,7 @@ int lch_encode_host(lch_ctx *c, const uint16_t *host_msg, int64_t stride_in, uin
                     int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len, int64_t chunk,
                     void *stream) {
   if (!c || !host_msg || batch < 0 || chunk < 0 || packet_len < 0) return LCH_EINVAL;
+  std::lock_guard<std::mutex> hg(c->host_mu);
   const int64_t n = int64_t(c->t.order), pkt = packet_len;
   if (k < 1 || k > n || stride_in < k || (k < n && (!host_parity || stride_out < n - k))) return LCH_EINVAL;
   if (pkt && (pkt % GROUP || batch % pkt)) return LCH_EINVAL;
@@ -1465,6 +1474,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
                     int64_t packet_len, int64_t chunk, void *stream) {
   if (!c || !host_rx || !host_bits || !host_out || batch < 0 || chunk < 0 || packet_len < 0)
     return LCH_EINVAL;
+  std::lock_guard<std::mutex> hg(c->host_mu);
   const int64_t n = int64_t(c->t.order), pkt = packet_len;
   if (k < 1 || k > n || stride_in < n || stride_out < k) return LCH_EINVAL;
   if (pkt && (pkt % GROUP || batch % pkt)) return LCH_EINVAL;

@@ -83,3 +83,29 @@ def test_random_codec(lch, bt8, orc8, seed):
     _lib.check(_lib.lib.lch_decode_k(bt8.ctx.handle, dev(rx).data_ptr(), n, bits.data_ptr(), int(shared),
                                      out.data_ptr(), k, B, k, 0, None, _lib.stream_ptr()))
     np.testing.assert_array_equal(host(out), msg)
+
+
+def test_per_codeword_decode_in_lane_chunks(lch, bt8, orc8):
+    """A scratch budget below the batch splits per-codeword decodes into lane
+    chunks (phi, -log Pi' and the bit-sliced intermediates are per codeword)."""
+    import torch
+    from paper_1404_3458_b200 import _lib
+    from paper_1404_3458_b200.gen import mask_to_bits
+    from paper_1404_3458_b200.stripe import set_scratch_limit
+    n, k, B = 256, 100, 3000
+    rng = np.random.default_rng(9)
+    msg = rng.integers(0, 256, (B, k)).astype(np.uint16)
+    cw = np.concatenate([msg, orc8.encode_any_batch(k, msg, nthreads=8)], axis=1)
+    masks = np.zeros((B, n), bool)
+    for row in masks:
+        row[rng.choice(n, int(rng.integers(0, n - k + 1)), replace=False)] = True
+    rx = np.where(masks, 7, cw).astype(np.uint16)
+    bits = mask_to_bits(torch.from_numpy(masks).to("cuda")).contiguous()
+    out = torch.empty((B, k), dtype=torch.int16, device="cuda")
+    try:
+        set_scratch_limit(bt8, 1 << 20)
+        _lib.check(_lib.lib.lch_decode_k(bt8.ctx.handle, dev(rx).data_ptr(), n, bits.data_ptr(), 0,
+                                         out.data_ptr(), k, B, k, 0, None, _lib.stream_ptr()))
+    finally:
+        set_scratch_limit(bt8, 4 << 30)
+    np.testing.assert_array_equal(host(out), msg)

@@ -209,14 +209,18 @@ struct GF {
     for (int b = 0; b < R; ++b) p[b] = v[b];
 #pragma unroll
     for (int t = 0; t < R; ++t) {
+      // x * p for the next bit is computed ahead of this bit's branch, so
+      // its tap XORs are ready by the time the next body reads them
+      uint32_t q[R];
+      if (t + 1 < R) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) q[b] = xor_set(p, s1(b));
+      }
       if ((f >> t) & 1u) {
 #pragma unroll
         for (int b = 0; b < R; ++b) u[b] ^= p[b];
       }
       if (t + 1 < R) {
-        uint32_t q[R];
-#pragma unroll
-        for (int b = 0; b < R; ++b) q[b] = xor_set(p, s1(b));
 #pragma unroll
         for (int b = 0; b < R; ++b) p[b] = q[b];
       }

@@ -1536,6 +1536,77 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
                                              k, 0, counts.data(), stream);
                          });
   }
+  int64_t min_erased = counts.empty() ? 0 : counts[0];
+  for (int64_t v : counts) min_erased = std::min(min_erased, v);
+  // packing pays only when a large share of the packets is erased (the host
+  // copy of the survivors then costs less than moving the erased ones)
+  if (pkt && 5 * min_erased >= 2 * n && !std::getenv("LCH_NO_COMPACT")) {
+    // Packet layout (stripe groups): erasures are whole packets, so only the
+    // surviving packets cross PCIe -- the host packs them (memcpy per packet
+    // on the worker pool) into page-locked staging, the device scatters them
+    // back to their positions (erased packets read as zero).
+    int64_t minc = counts[0];
+    for (int64_t v : counts) minc = std::min(minc, v);
+    const int64_t msurv = std::max<int64_t>(n - minc, 1);
+    const size_t pkt_bytes = size_t(pkt) * 2;
+    HostPool &pool = host_pool(c);
+    std::vector<HostArray> cins(1);
+    cins[0].row_bytes = size_t(msurv) * pkt_bytes;
+    cins[0].prep = [&](int64_t r0, int64_t nr, uint8_t *stg) {
+      for (int64_t g = r0; g < r0 + nr; ++g) {
+        const uint32_t *gb = host_bits + (shared ? 0 : g * words);
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(host_rx) + size_t(g) * size_t(stride_in) * pkt_bytes;
+        uint8_t *dst = stg + size_t(g - r0) * size_t(msurv) * pkt_bytes;
+        // block prefix of survivors, then copy blocks of positions in parallel
+        constexpr int64_t BLK = 256;
+        const int64_t nblk = (n + BLK - 1) / BLK;
+        std::vector<int64_t> pre(static_cast<size_t>(nblk) + 1, 0);
+        for (int64_t bI = 0; bI < nblk; ++bI) {
+          int64_t cnt = 0;
+          for (int64_t j = bI * BLK; j < std::min(n, (bI + 1) * BLK); ++j) cnt += !((gb[j >> 5] >> (j & 31)) & 1u);
+          pre[size_t(bI) + 1] = pre[size_t(bI)] + cnt;
+        }
+        pool.run(nblk, 1, [&](int64_t lo, int64_t hi) {
+          for (int64_t bI = lo; bI < hi; ++bI) {
+            int64_t q = pre[size_t(bI)];
+            for (int64_t j = bI * BLK; j < std::min(n, (bI + 1) * BLK); ++j)
+              if (!((gb[j >> 5] >> (j & 31)) & 1u))
+                std::memcpy(dst + size_t(q++) * pkt_bytes, src + size_t(j) * pkt_bytes, pkt_bytes);
+          }
+        });
+      }
+    };
+    HostArray cout;
+    cout.dst = reinterpret_cast<uint8_t *>(host_out);
+    cout.row_bytes = size_t(k) * pkt_bytes;
+    cout.pitch = size_t(stride_out) * pkt_bytes;
+    return host_pipeline(c, s, rows, chunk, cins, cout,
+                         [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr) {
+                           Scratch cs(s);
+                           const int64_t npat = shared ? 1 : nr;
+                           std::vector<int32_t> rank(size_t(npat) * size_t(n), -1);
+                           for (int64_t g = 0; g < npat; ++g) {
+                             const uint32_t *gb = host_bits + (shared ? 0 : (r0 + g) * words);
+                             for (int64_t j = 0, q = 0; j < n; ++j)
+                               if (!((gb[j >> 5] >> (j & 31)) & 1u)) rank[size_t(g * n + j)] = int32_t(q++);
+                           }
+                           int32_t *d_rank = nullptr;
+                           uint32_t *d_bits = d_shared;
+                           uint16_t *full = nullptr;
+                           LCH_TRY(cs.alloc(d_rank, rank.size()));
+                           LCH_TRY(upload_small(c, d_rank, rank.data(), rank.size() * 4, s));
+                           if (!shared) {
+                             LCH_TRY(cs.alloc(d_bits, size_t(nr * words)));
+                             LCH_TRY(upload_small(c, d_bits, host_bits + r0 * words, size_t(nr * words) * 4, s));
+                           }
+                           LCH_TRY(cs.alloc(full, size_t(nr) * size_t(n) * size_t(pkt)));
+                           LCH_TRY(cu(launch_expand_packets(reinterpret_cast<const uint16_t *>(d[0]), msurv, d_rank,
+                                                            shared ? 0 : n, full, n, pkt, nr, s)));
+                           c->launches++;
+                           return decode_any(c, full, n, d_bits, shared, reinterpret_cast<uint16_t *>(o), k,
+                                             nr * pkt, k, pkt, counts.data() + (shared ? 0 : r0), stream);
+                         });
+  }
   std::vector<HostArray> ins(shared ? 1 : 2);
   ins[0].src = reinterpret_cast<const uint8_t *>(host_rx);
   ins[0].row_bytes = in_row;

@@ -1339,6 +1339,27 @@ cudaError_t launch_expand_rows(const uint16_t *comp, int64_t comp_stride, const 
   return cudaGetLastError();
 }
 
+__global__ void expand_packets_kernel(const uint4 *comp, int64_t comp_pos, const int32_t *rank,
+                                      int64_t rank_stride, uint4 *full, int64_t n, int64_t pk4, int64_t groups) {
+  const int64_t total = groups * n * pk4;  // in uint4 (8 symbols)
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t t = i % pk4, rest = i / pk4, j = rest % n, g = rest / n;
+    const int32_t q = __ldg(rank + g * rank_stride + j);
+    full[i] = q >= 0 ? __ldcs(comp + (g * comp_pos + q) * pk4 + t) : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+cudaError_t launch_expand_packets(const uint16_t *comp, int64_t comp_pos, const int32_t *rank,
+                                  int64_t rank_stride, uint16_t *full, int64_t n, int64_t pkt, int64_t groups,
+                                  cudaStream_t s) {
+  const int64_t pk4 = pkt / 8;
+  expand_packets_kernel<<<grid_for(groups * n * pk4), 256, 0, s>>>(
+      reinterpret_cast<const uint4 *>(comp), comp_pos, rank, rank_stride, reinterpret_cast<uint4 *>(full), n,
+      pk4, groups);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pointwise_mul(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
                                  const uint16_t *log, const uint16_t *exp, uint32_t m, cudaStream_t s) {
   pointwise_mul_kernel<<<grid_for(count), 256, 0, s>>>(a, b, out, count, log, exp, m);

@@ -177,6 +177,10 @@ cudaError_t launch_xor_views(uint16_t *out, int64_t so, const uint16_t *a, int64
 // full[r][j] = rank[j] >= 0 ? comp[r][rank[j]] : 0 (survivor rows -> n-wide rows)
 cudaError_t launch_expand_rows(const uint16_t *comp, int64_t comp_stride, const int32_t *rank, uint16_t *full,
                                int64_t n, int64_t rows, cudaStream_t s);
+// packets: full[g][j][P] = rank[g*rank_stride + j] >= 0 ? comp[g][rank][P] : 0
+cudaError_t launch_expand_packets(const uint16_t *comp, int64_t comp_pos, const int32_t *rank,
+                                  int64_t rank_stride, uint16_t *full, int64_t n, int64_t pkt, int64_t groups,
+                                  cudaStream_t s);
 cudaError_t launch_pointwise_mul(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
                                  const uint16_t *log, const uint16_t *exp, uint32_t m, cudaStream_t s);
 cudaError_t launch_stripes_to_packets(const uint8_t *bytes, int64_t len, int w, int64_t k, int64_t S,

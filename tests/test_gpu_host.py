@@ -112,11 +112,13 @@ def test_host_r16_matches_device(lch, bt16):
     assert torch.equal(hout, dmsg.cpu())
 
 
-def test_packet_host_pipeline(lch, bt8):
-    """Packet layout through the host pipeline (rows = stripe groups)."""
+@pytest.mark.parametrize("k", [192, 100])
+def test_packet_host_pipeline(lch, bt8, k):
+    """Packet layout through the host pipeline (rows = stripe groups); k = 100
+    erases > 40 % of the packets, so surviving packets are packed on the host."""
     import torch
     from paper_1404_3458_b200 import _lib, gen
-    P, G, k, n = 1024, 5, 192, 256
+    P, G, n = 1024, 5, 256
     sc = lch.StripeCodec(bt8, k, P)
     msg = gen.packets(bt8.ctx, 31, 0, G, k, P)
     par = sc.encode(msg)

@@ -1451,7 +1451,7 @@ int lch_encode_host(lch_ctx *c, const uint16_t *host_msg, int64_t stride_in, uin
   // rows: codewords, or stripe groups of pkt lanes
   const int64_t rows = pkt ? batch / pkt : batch, lanes_per_row = pkt ? pkt : 1;
   const size_t in_row = size_t(k * lanes_per_row) * 2, out_row = size_t((n - k) * lanes_per_row) * 2;
-  if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / std::max(in_row, out_row)));
+  if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(32) << 20) / std::max(in_row, out_row)));
   chunk = std::min(chunk, rows);
   std::vector<HostArray> ins(1);
   ins[0].src = reinterpret_cast<const uint8_t *>(host_msg);

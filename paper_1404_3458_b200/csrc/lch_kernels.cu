@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
     if (p.in_mode == IO_RAW) {
-      finish_tile_raw<R>(smem, TP);
+      if (!(p.dbg & 128)) finish_tile_raw<R>(smem, TP);
       __syncthreads();
     }
     if (p.npre) {

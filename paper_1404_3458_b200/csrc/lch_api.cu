@@ -204,6 +204,11 @@ int build_rounds(const Plan &pl, PassParams &p) {
     cur.nw = 0;
     for (int b = 0; b < tpb; ++b)
       if (b != cur.m0 && b != cur.m1) cur.obit[cur.nw++] = b;
+    for (int w = 0; w < NWARP; ++w) {
+      int q = 0;
+      for (int j = 0; j < cur.nw; ++j) q |= ((w >> j) & 1) << cur.obit[j];
+      cur.q0w[w] = uint8_t(q);
+    }
     cur.op_end = p.nops;
     // a pair's factor depends on the position bits above its level only
     // (transform.py:123), so both pairs of an op share it when the round's
@@ -301,6 +306,12 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     p.tpb = int(pl.bits.size());
     p.lgH = lgH;
     fill_bits(pl.bits, lgH, p.gbit, p.nnb, p.nbit);
+    {
+      std::vector<int> sb(pl.bits);
+      std::sort(sb.begin(), sb.end());
+      for (size_t m = 0; m < sb.size(); ++m) p.ins_mask[m] = (1u << sb[m]) - 1u;
+    }
+    p.lgnt = lgH - p.tpb;
     p.batch = batch;
     p.ngroups = ngroups;
     p.pkt = pkt;

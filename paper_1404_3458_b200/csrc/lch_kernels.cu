@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // the butterfly factors and their digit tests live in uniform registers
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int TP = 1 << p.tpb;
-  const int ntile = 1 << (p.lgH - p.tpb);
+  const int ntile = 1 << p.lgnt;
   const int total = ntile * p.ngroups;
   int tl = blockIdx.x;
   if (tl >= total) return;
@@ -518,13 +518,19 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     for (int m = 0; m < p.tpb; ++m) o |= ((uint32_t(tid) >> m) & 1u) << p.gbit[m];
     tpos[tid] = o;
   }
+  // tile base: the tile index spread over the non-tile bits (ascending), i.e.
+  // a zero inserted at every tile bit
   auto base_of = [&](int lin) {
-    const uint32_t t = uint32_t(lin % ntile);
-    uint32_t b = 0;
-    for (int i = 0; i < p.nnb; ++i) b |= ((t >> i) & 1u) << p.nbit[i];
+    uint32_t b = uint32_t(lin) & uint32_t(ntile - 1);
+#pragma unroll
+    for (int m = 0; m < TPB_MAX; ++m)
+      if (m < p.tpb) {
+        const uint32_t lm = p.ins_mask[m];
+        b = ((b & ~lm) << 1) | (b & lm);
+      }
     return b;
   };
-  int g = tl / ntile;
+  int g = tl >> p.lgnt;
   uint32_t base = base_of(tl);
   if (tid == 0) {
     mbar_init(&bar, 1);
@@ -567,8 +573,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       const bool has1 = rr.m1 >= 0;
       const int M1 = has1 ? (1 << rr.m1) : 0;
       const bool active = warp < (1 << rr.nw);
-      int q0 = 0;
-      for (int j = 0; j < rr.nw; ++j) q0 |= ((warp >> j) & 1) << rr.obit[j];
+      const int q0 = rr.q0w[warp];
       uint32_t a0[R], a1[R], a2[R], a3[R];
       if (active && !(p.dbg & 32)) {
         Blk<R>::load(bsm + q0 * U4, lane, a0);
@@ -583,7 +588,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         __syncthreads();
         if (has_next) {
           const uint32_t nb = base_of(next);
-          issue_tile<R>(p, smem, tpos, next / ntile, nb, TP, &bar);
+          issue_tile<R>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
           if (!(p.dbg & 64)) nfl.fetch(p, tpos, nb);
         }
       }
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       __syncthreads();
       if (has_next) {
         const uint32_t nb = base_of(next);
-        issue_tile<R>(p, smem, tpos, next / ntile, nb, TP, &bar);
+        issue_tile<R>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
         FactorLoader fl;
         if (!(p.dbg & 64)) {
           fl.fetch(p, tpos, nb);
@@ -751,7 +756,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     __syncthreads();
     fb ^= 1;
     tl = next;
-    g = tl / ntile;
+    g = tl >> p.lgnt;
     base = base_of(tl);
   }
 }

@@ -38,6 +38,7 @@ struct PassRound {
   int nw;
   int obit[TPB_MAX];
   int op_begin, op_end;   // butterfly ops of the round in ops[]
+  uint8_t q0w[NWARP];     // warp w's first tile position (obit[] spread of w), precomputed
   int shape;              // 0 general; 1: one op along m0; 2: one along m0 then one along m1
 };
 
@@ -83,6 +84,9 @@ struct PassParams {
   int lgH;               // positions in the buffers = 2^lgH
   int nnb;               // non-tile bits
   int nbit[16];          // non-tile bit i -> global position bit
+  uint32_t ins_mask[TPB_MAX];  // (1 << g) - 1 for the tile bits g, ascending: tile base =
+                               // tile index with a zero inserted at each g
+  int lgnt;              // log2 of the tiles per group (lgH - tpb)
   int64_t batch;
   int ngroups;           // 1024-lane batch groups
   int64_t pkt;           // stripe-group size in batch lanes (table rows), 0 = none

@@ -328,7 +328,8 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
       p.gt_lgH = gt_lgH;
     }
     {
-      static const int dbg = std::getenv("LCH_DBG_PASS") ? std::atoi(std::getenv("LCH_DBG_PASS")) : 0;
+      static const int dbg =
+          std::getenv("LCH_DBG_PASS") ? int(std::strtoul(std::getenv("LCH_DBG_PASS"), nullptr, 0)) : 0;
       p.dbg = dbg;
     }
     for (int l = 0; l <= c->t.levels && l < 17; ++l) p.w_hat_off[l] = c->t.w_hat_off[l];

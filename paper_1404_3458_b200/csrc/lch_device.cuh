@@ -199,6 +199,87 @@ struct GF {
     lazy_reduce(u, h);
   }
 
+  // Nested 2-bit digits: per digit (bits t, t+1) two warp-uniform branches,
+  // as many as the 1-bit form, but a digit with both bits set adds p + x p
+  // in ONE 3-input LOP3 per plane (u ^= p ^ q): 3/4 * 16 body ops per digit
+  // instead of 2 * 1/2 * 16.  p and q = x p are both computed every digit
+  // (the same tap XORs the 1-bit form spends), so no body does extra work.
+  __device__ __forceinline__ static void mul_acc_n2(uint32_t (&u)[R], const uint32_t (&v)[R],
+                                                    uint32_t f) {
+    uint32_t p[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) p[b] = v[b];
+#pragma unroll
+    for (int t = 0; t < R; t += 2) {
+      uint32_t q[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) q[b] = xor_set(p, s1(b));
+      if ((f >> t) & 1u) {
+        if ((f >> (t + 1)) & 1u) {
+#pragma unroll
+          for (int b = 0; b < R; ++b) u[b] = lop3_xor(u[b], p[b], q[b]);
+        } else {
+#pragma unroll
+          for (int b = 0; b < R; ++b) u[b] ^= p[b];
+        }
+      } else if ((f >> (t + 1)) & 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] ^= q[b];
+      }
+      if (t + 2 < R) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) p[b] = xor_set(q, s1(b));
+      }
+    }
+  }
+  __device__ __forceinline__ static void mul_acc2_n2(uint32_t (&u0)[R], const uint32_t (&v0)[R],
+                                                     uint32_t (&u1)[R], const uint32_t (&v1)[R],
+                                                     uint32_t f) {
+    uint32_t p0[R], p1[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      p0[b] = v0[b];
+      p1[b] = v1[b];
+    }
+#pragma unroll
+    for (int t = 0; t < R; t += 2) {
+      uint32_t q0[R], q1[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        q0[b] = xor_set(p0, s1(b));
+        q1[b] = xor_set(p1, s1(b));
+      }
+      if ((f >> t) & 1u) {
+        if ((f >> (t + 1)) & 1u) {
+#pragma unroll
+          for (int b = 0; b < R; ++b) {
+            u0[b] = lop3_xor(u0[b], p0[b], q0[b]);
+            u1[b] = lop3_xor(u1[b], p1[b], q1[b]);
+          }
+        } else {
+#pragma unroll
+          for (int b = 0; b < R; ++b) {
+            u0[b] ^= p0[b];
+            u1[b] ^= p1[b];
+          }
+        }
+      } else if ((f >> (t + 1)) & 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] ^= q0[b];
+          u1[b] ^= q1[b];
+        }
+      }
+      if (t + 2 < R) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          p0[b] = xor_set(q0, s1(b));
+          p1[b] = xor_set(q1, s1(b));
+        }
+      }
+    }
+  }
+
 #ifndef LCH_MUL_2BIT
   // 1-bit digits: one warp-uniform branch per bit of f (fewer taken
   // branches than the 2-bit digits below: measured 4-5% faster passes)

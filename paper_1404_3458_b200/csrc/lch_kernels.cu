@@ -431,8 +431,10 @@ __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], ui
     F::mul_acc_lazy(u, v, f);
 #elif defined(LCH_MUL_LAZY2)
     F::mul_acc_lazy2(u, v, f);
-#elif !defined(LCH_MUL_2BIT)
+#elif defined(LCH_MUL_1BIT)
     F::mul_acc_1(u, v, f);
+#elif !defined(LCH_MUL_2BIT)
+    F::mul_acc_n2(u, v, f);
 #else
     F::mul_acc(u, v, f);
 #endif
@@ -450,8 +452,10 @@ __device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R],
     F::xor_into(v1, u1);
   }
   if (f) {
-#ifndef LCH_MUL_2BIT
+#if defined(LCH_MUL_1BIT)
     F::mul_acc2_1(u0, v0, u1, v1, f);
+#elif !defined(LCH_MUL_2BIT)
+    F::mul_acc2_n2(u0, v0, u1, v1, f);
 #else
     F::mul_acc2(u0, v0, u1, v1, f);
 #endif
@@ -484,6 +488,7 @@ struct FactorLoader {
         const int qu = ((pp >> m) << (m + 1)) | (pp & ((1 << m) - 1));
         const int lvl = op.level;
         v[k] = uint32_t(__ldg(p.w_hat + p.w_hat_off[lvl] + ((base | tpos[qu]) >> (lvl + 1)))) ^ op.hs;
+        if (p.dbg & 256) v[k] = uint32_t(p.dbg) >> 16;  // experiment: one forced factor
         slot[k] = o * (1 << TPB_MAX) + qu;
       }
     }

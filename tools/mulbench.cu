@@ -1,5 +1,8 @@
-// Microbenchmark: throughput of the bit-sliced multiply (GF::mul_acc_1) (warp-uniform
-// factors) with W words per lane sharing each factor.  Experiments only.
+// Microbenchmark: throughput of the bit-sliced multiply (GF::mul_acc_n2,
+// warp-uniform factors) against resident warps per SM; W = lane-words per
+// thread (W = 2 shares each factor's branches between two words, as
+// mul_acc2_n2 does).  Experiments only: nvcc -O3 -gencode
+// arch=compute_100a,code=sm_100a tools/mulbench.cu -o tools/mulbench
 #include <cstdint>
 #include <cstdio>
 #include "../paper_1404_3458_b200/csrc/lch_device.cuh"
@@ -14,10 +17,10 @@ __global__ void __launch_bounds__(256) k(const uint32_t *fac, uint32_t *out, int
   for (int it = 0; it < iters; ++it) {
     const uint32_t f = fac[(blockIdx.x * 8 + warp + it * 7) & 4095];
     if (W == 1) {
-      F::mul_acc_1(u[0], v[0], f);
+      F::mul_acc_n2(u[0], v[0], f);
       for (int b = 0; b < 16; ++b) v[0][b] ^= u[0][b];
     } else {
-      F::mul_acc2_1(u[0], v[0], u[W - 1], v[W - 1], f);
+      F::mul_acc2_n2(u[0], v[0], u[W - 1], v[W - 1], f);
       for (int b = 0; b < 16; ++b) { v[0][b] ^= u[0][b]; v[W-1][b] ^= u[W-1][b]; }
     }
   }
@@ -37,7 +40,7 @@ int main() {
   cudaEventCreate(&a); cudaEventCreate(&b);
   const int iters = 2000;
   for (int W = 1; W <= 2; ++W)
-    for (int ctas_per_sm = 1; ctas_per_sm <= 4; ctas_per_sm *= 2) {
+    for (int ctas_per_sm = 1; ctas_per_sm <= 8; ctas_per_sm *= 2) {
       const int grid = 148 * ctas_per_sm;
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(a);
@@ -47,7 +50,7 @@ int main() {
       }
       float ms; cudaEventElapsedTime(&ms, a, b);
       const double muls = double(grid) * 256 * iters * 32 * W;
-      printf("W=%d ctas/SM=%d: %.3f ms  %.2f T symbol-muls/s (%s)\n", W, ctas_per_sm, ms,
+      printf("W=%d warps/SM=%d: %.3f ms  %.2f T symbol-muls/s (%s)\n", W, ctas_per_sm * 8, ms,
              muls / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
     }
   return 0;

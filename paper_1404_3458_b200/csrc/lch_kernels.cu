@@ -954,43 +954,62 @@ __device__ __forceinline__ void wht16(uint32_t (&v)[16]) {
   for (int e = 0; e < 16; ++e) v[e] = fold16(fold16(v[e]));
 }
 
+// Shared-memory layout of the 2^16 residues: uint16 pairs (positions 2w,
+// 2w + 1) in 32-bit words, word w stored at lsw(w) = w ^ (((w >> 7) & 3) << 3)
+// so that the rounds over position bits 4-7 (whose lanes step the word index
+// by 2^7) spread over all banks; the swizzle moves whole 32-byte chunks, so
+// the 16-position slot vectors of the first/last round stay contiguous.
+__device__ __forceinline__ uint32_t lsw(uint32_t w) { return w ^ (((w >> 7) & 3u) << 3); }
+
 __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant__ FwhtParams p) {
   extern __shared__ uint16_t sv[];  // 2^16 residues
+  uint32_t *const sw = reinterpret_cast<uint32_t *>(sv);
   constexpr uint32_t M = 0xFFFFu;
   const int64_t vec = blockIdx.x;
   const uint32_t *bits = p.bits + vec * 2048;
   const int tid = threadIdx.x;
-  auto pos = [](int slot, int b0, int e) -> uint32_t {
-    const uint32_t lo = uint32_t(slot) & ((1u << b0) - 1u), hi = uint32_t(slot) >> b0;
-    return (hi << (b0 + 4)) | (uint32_t(e) << b0) | lo;
-  };
-  // G0 of the first transform, from the bitmask (16 bits per slot)
+  // G0 of the first transform, from the bitmask (16 bits per slot), stored as
+  // two 16-byte vectors per slot
   for (int slot = tid; slot < 4096; slot += LOC_NT) {
     const uint32_t w = (bits[slot >> 1] >> (16 * (slot & 1))) & 0xFFFFu;
     uint32_t v[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = (w >> e) & 1u;
     wht16(v);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) sv[(slot << 4) | e] = uint16_t(v[e]);
+    uint4 *dst = reinterpret_cast<uint4 *>(sw + lsw(uint32_t(slot) << 3));
+    dst[0] = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+    dst[1] = make_uint4(v[8] | (v[9] << 16), v[10] | (v[11] << 16), v[12] | (v[13] << 16),
+                        v[14] | (v[15] << 16));
   }
   __syncthreads();
+  // A round over position bits b0..b0+3 (b0 >= 1): a thread takes the two
+  // slots that differ in position bit 0 together, one 32-bit word per pair.
   auto round = [&](int b0, bool mul) {
-    for (int slot = tid; slot < 4096; slot += LOC_NT) {
-      uint32_t v[16];
+    const int lb = b0 - 1;  // word-index bits below the round's bits
+    for (int sp = tid; sp < 2048; sp += LOC_NT) {
+      const uint32_t lo = uint32_t(sp) & ((1u << lb) - 1u), hi = uint32_t(sp) >> lb;
+      const uint32_t w0 = (hi << (lb + 4)) | lo;
+      uint32_t va[16], vb[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = sv[pos(slot, b0, e)];
-      wht16(v);
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t x = sw[lsw(w0 | (uint32_t(e) << lb))];
+        va[e] = x & 0xFFFFu;
+        vb[e] = x >> 16;
+      }
+      wht16(va);
+      wht16(vb);
       if (mul) {
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const uint32_t prod = v[e] * __ldg(p.post_mul + pos(slot, b0, e));
-          v[e] = fold16(fold16(prod));
+          const uint2 m = __ldg(reinterpret_cast<const uint2 *>(p.post_mul) + (w0 | (uint32_t(e) << lb)));
+          va[e] = fold16(fold16(va[e] * m.x));
+          vb[e] = fold16(fold16(vb[e] * m.y));
         }
-        wht16(v);
+        wht16(va);
+        wht16(vb);
       }
 #pragma unroll
-      for (int e = 0; e < 16; ++e) sv[pos(slot, b0, e)] = uint16_t(v[e]);
+      for (int e = 0; e < 16; ++e) sw[lsw(w0 | (uint32_t(e) << lb))] = va[e] | (vb[e] << 16);
     }
     __syncthreads();
   };
@@ -1003,7 +1022,7 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
   const uint32_t *bits_e = p.bits_e ? p.bits_e + vec * 2048 : nullptr;
   for (int slot = tid; slot < 4096; slot += LOC_NT) {
     uint32_t v[16];
-    const uint4 *src = reinterpret_cast<const uint4 *>(sv + (slot << 4));
+    const uint4 *src = reinterpret_cast<const uint4 *>(sw + lsw(uint32_t(slot) << 3));
     const uint4 x0 = src[0], x1 = src[1];
     const uint32_t w8[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
@@ -1017,6 +1036,21 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
       const uint4 *rxv = reinterpret_cast<const uint4 *>(p.rx + vec * p.rx_stride + j0);
       const uint4 r0 = __ldcs(rxv), r1 = __ldcs(rxv + 1);
       const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      // phi = rx * Pi-bar through log/exp: all 16 log gathers, then all 16
+      // exp gathers, so each thread keeps 16 independent loads in flight
+      uint32_t lr[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t r = (rw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+        lr[e] = r ? uint32_t(__ldg(p.log + r)) : 0u;
+      }
+      uint32_t ex[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        uint32_t t = lr[e] + v[e];
+        t = t >= M ? t - M : t;
+        ex[e] = __ldg(p.exp + t);
+      }
       uint32_t o[8];
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
@@ -1025,13 +1059,8 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
         for (int q = 0; q < 2; ++q) {
           const int e = 2 * h + q;
           const uint32_t r = (rw[h] >> (16 * q)) & 0xFFFFu;
-          uint32_t ph = 0;
-          if (!((er >> e) & 1u) && r) {
-            uint32_t t = uint32_t(__ldg(p.log + r)) + v[e];
-            t = t >= M ? t - M : t;
-            ph = __ldg(p.exp + t);
-          }
-          pair |= ph << (16 * q);
+          const bool keep = !((er >> e) & 1u) && r;
+          pair |= (keep ? ex[e] : 0u) << (16 * q);
         }
         o[h] = pair;
       }
@@ -1040,10 +1069,19 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
       __stcs(dst + 1, make_uint4(o[4], o[5], o[6], o[7]));
       if (j0 < p.k) {
         uint16_t *pl = p.pinv_log + vec * p.k;
+        uint32_t pv[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t j = j0 + e;
-          if (j < p.k) pl[j] = ((er >> e) & 1u) ? uint16_t(v[e] ? M - v[e] : 0u) : uint16_t(0);
+        for (int e = 0; e < 16; ++e) pv[e] = ((er >> e) & 1u) ? (v[e] ? M - v[e] : 0u) : 0u;
+        if (j0 + 16 <= p.k && (p.k & 7) == 0) {
+          uint4 *pd = reinterpret_cast<uint4 *>(pl + j0);
+          pd[0] = make_uint4(pv[0] | (pv[1] << 16), pv[2] | (pv[3] << 16), pv[4] | (pv[5] << 16),
+                             pv[6] | (pv[7] << 16));
+          pd[1] = make_uint4(pv[8] | (pv[9] << 16), pv[10] | (pv[11] << 16), pv[12] | (pv[13] << 16),
+                             pv[14] | (pv[15] << 16));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (j0 + e < p.k) pl[j0 + e] = uint16_t(pv[e]);
         }
       }
     } else {

@@ -342,13 +342,33 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
         const uint32_t eb = (mb[pos0 >> 5] >> (pos0 & 31)) & 0xFFu;
         uint32_t *vv = &val.x;
         if (io.pinv_log && eb) {
+          // erased j: computed * alpha^pinv_log(b, j) (division by Pi'(j),
+          // rs.py:141-148); the 8 log gathers, then the 8 exp gathers, are
+          // issued together, and both exponents are < mord so one conditional
+          // subtraction reduces their sum
           const uint16_t *pl = io.pinv_log + b * io.pinv_stride + pos0;
+          uint32_t pw[4];
+          if (((io.pinv_stride & 7) | (reinterpret_cast<uintptr_t>(io.pinv_log) & 15)) == 0) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(pl));
+            pw[0] = q.x, pw[1] = q.y, pw[2] = q.z, pw[3] = q.w;
+          } else {
+#pragma unroll
+            for (int h = 0; h < 4; ++h) pw[h] = uint32_t(__ldg(pl + 2 * h)) | (uint32_t(__ldg(pl + 2 * h + 1)) << 16);
+          }
+          uint32_t lg[8];
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const uint32_t x = (vv[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
+            lg[h] = (((eb >> h) & 1u) && x) ? uint32_t(__ldg(io.log_tab + x)) : 0u;
+          }
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
             if (!((eb >> h) & 1u)) continue;
             const uint32_t sh = 16 * (h & 1);
             const uint32_t x = (vv[h >> 1] >> sh) & 0xFFFFu;
-            const uint32_t y = x ? io.exp_tab[(uint32_t(__ldg(io.log_tab + x)) + __ldg(pl + h)) % io.mord] : 0u;
+            uint32_t t = lg[h] + ((pw[h >> 1] >> sh) & 0xFFFFu);
+            t = t >= io.mord ? t - io.mord : t;
+            const uint32_t y = x ? uint32_t(__ldg(io.exp_tab + t)) : 0u;
             vv[h >> 1] = (vv[h >> 1] & ~(0xFFFFu << sh)) | (y << sh);
           }
         }
@@ -382,7 +402,8 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
             v = io.pkt ? io.merge_src[((b / io.pkt) * io.merge_stride + pos) * io.pkt + b % io.pkt]
                        : io.merge_src[b * io.merge_stride + pos];
           } else if (io.pinv_log && v) {
-            v = io.exp_tab[(uint32_t(io.log_tab[v]) + io.pinv_log[b * io.pinv_stride + pos]) % io.mord];
+            uint32_t t = uint32_t(io.log_tab[v]) + io.pinv_log[b * io.pinv_stride + pos];
+            v = io.exp_tab[t >= io.mord ? t - io.mord : t];
           }
         }
         *const_cast<uint16_t *>(raw_addr(io, b, pos)) = v;

@@ -20,7 +20,7 @@ rx[:, mask[0]] = 0
 h_msg, h_rx = msg.cpu().pin_memory(), rx.cpu().pin_memory()
 h_par = torch.empty((B, K), dtype=torch.int16, pin_memory=True)
 h_out = torch.empty((B, K), dtype=torch.int16, pin_memory=True)
-for ce, cd in [(0, 0), (512, 256), (256, 128), (2048, 1024), (1024, 256), (512, 512)]:
+for ce, cd in [(0, 0), (1024, 1024), (512, 1024), (2048, 1024), (1024, 2048), (0, 1024), (512, 512)]:
     def step():
         encode_host(cp, bt, h_msg, h_par, ce)
         decode_host(cp, bt, h_rx, bits, h_out, cd)

@@ -808,9 +808,12 @@ __global__ void __launch_bounds__(GNT, 2) gather_kernel(const __grid_constant__ 
   const int nout = 1 << nlow;
   const int lw = p.lwpc, WPC = 1 << lw;
   const int wblocks = 32 >> lw;
-  const int g = blockIdx.y / wblocks, w0 = (blockIdx.y - g * wblocks) * WPC;
+  // blockIdx.x enumerates (group, lane-word block) fastest, so the CTAs that
+  // read the different 64-byte lane-word slices of the same 2 KB position
+  // blocks are scheduled together (DRAM row locality)
+  const int g = blockIdx.x / wblocks, w0 = (blockIdx.x - g * wblocks) * WPC;
   uint4 *ytile = smem;
-  const uint32_t t = blockIdx.x;
+  const uint32_t t = blockIdx.y;
   uint32_t base = 0;
   for (int i = 0; i < p.nnb; ++i) base |= ((t >> i) & 1u) << p.nbit[i];
   const uint32_t hout = 1u << p.lgH_out;
@@ -1258,7 +1261,7 @@ cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s) {
   static std::atomic<uint64_t> done{0};
   cudaError_t e = smem_optin(gather_kernel<R, POLY>, int(GATHER_SMEM_MAX), done);
   if (e != cudaSuccess) return e;
-  dim3 grid(1u << (p.lgH_in - p.nbits), unsigned(ngroups) * (32u >> p.lwpc));
+  dim3 grid(unsigned(ngroups) * (32u >> p.lwpc), 1u << (p.lgH_in - p.nbits));
   gather_kernel<R, POLY><<<grid, GNT, smem, s>>>(p);
   return cudaGetLastError();
 }

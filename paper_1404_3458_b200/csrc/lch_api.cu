@@ -414,10 +414,11 @@ struct DecodeEpi {
   uint16_t *phi = nullptr;
   uint16_t *pinv_log = nullptr;
   uint32_t k = 0;
+  bool pinv_val = false;  // out: the locator wrote 1 / Pi' values (r = 16 kernel), not logs
 };
 
 int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out, uint16_t *log_out,
-                 cudaStream_t s, const DecodeEpi *epi = nullptr) {
+                 cudaStream_t s, DecodeEpi *epi = nullptr) {
   const int r = c->t.r;
   const size_t n = size_t(1) << r;
   const bool aligned = !epi || (reinterpret_cast<uintptr_t>(epi->rx) % 16 == 0 &&
@@ -443,6 +444,7 @@ int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out
       p.phi = epi->phi;
       p.pinv_log = epi->pinv_log;
       p.k = epi->k;
+      epi->pinv_val = true;
     }
     LCH_TRY(cu(launch_locator16(p, s)));
     c->launches++;
@@ -1040,6 +1042,7 @@ static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in
     out0.bits_stride = n / 32;
     out0.pinv_log = pinv_log;
     out0.pinv_stride = kf;
+    out0.pinv_val = epi.pinv_val ? 1 : 0;
     out0.log_tab = c->d_log;
     out0.exp_tab = c->d_exp;
     out0.mord = c->t.m;

@@ -431,6 +431,27 @@ struct GF {
   }
 };
 
+// Product of two GF(2^16) symbols (polynomial basis, x^16 + x^12 + x^3 + x + 1,
+// field.py:100-129) without tables: a carry-less 16x16 multiply from 16
+// integer multiplies of bit-interleaved quarters (bits of a and b spaced 4
+// apart, so every partial coefficient stays below 16 and a product's parity
+// bits never collide), then four folds of the high half by the taps.
+__device__ __forceinline__ uint32_t gf16_mul(uint32_t a, uint32_t b) {
+  const uint32_t a0 = a & 0x1111u, a1 = a & 0x2222u, a2 = a & 0x4444u, a3 = a & 0x8888u;
+  const uint32_t b0 = b & 0x1111u, b1 = b & 0x2222u, b2 = b & 0x4444u, b3 = b & 0x8888u;
+  const uint32_t z0 = (a0 * b0) ^ (a1 * b3) ^ (a2 * b2) ^ (a3 * b1);
+  const uint32_t z1 = (a0 * b1) ^ (a1 * b0) ^ (a2 * b3) ^ (a3 * b2);
+  const uint32_t z2 = (a0 * b2) ^ (a1 * b1) ^ (a2 * b0) ^ (a3 * b3);
+  const uint32_t z3 = (a0 * b3) ^ (a1 * b2) ^ (a2 * b1) ^ (a3 * b0);
+  uint32_t z = (z0 & 0x11111111u) | (z1 & 0x22222222u) | (z2 & 0x44444444u) | (z3 & 0x88888888u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // degree 30 -> 26 -> 22 -> 18 -> 14
+    const uint32_t h = z >> 16;
+    z = (z & 0xFFFFu) ^ h ^ (h << 1) ^ (h << 3) ^ (h << 12);
+  }
+  return z;
+}
+
 // 32x32 bit-matrix transpose in registers: bit c of a[r] <-> bit r of a[c].
 // Stages 16 and 8 are byte permutes; 4, 2, 1 are masked swaps.
 __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {

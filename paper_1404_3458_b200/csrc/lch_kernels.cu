@@ -342,6 +342,7 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
         const uint32_t eb = (mb[pos0 >> 5] >> (pos0 & 31)) & 0xFFu;
         uint32_t *vv = &val.x;
         if (io.pinv_log && eb) {
+          bool eb_done = false;
           // erased j: computed * alpha^pinv_log(b, j) (division by Pi'(j),
           // rs.py:141-148); the 8 log gathers, then the 8 exp gathers, are
           // issued together, and both exponents are < mord so one conditional
@@ -355,14 +356,26 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
 #pragma unroll
             for (int h = 0; h < 4; ++h) pw[h] = uint32_t(__ldg(pl + 2 * h)) | (uint32_t(__ldg(pl + 2 * h + 1)) << 16);
           }
+          if constexpr (R == 16) {
+            if (io.pinv_val) {  // 1 / Pi' as values: table-free products
+#pragma unroll
+              for (int h = 0; h < 8; ++h) {
+                if (!((eb >> h) & 1u)) continue;
+                const uint32_t sh = 16 * (h & 1);
+                const uint32_t y = gf16_mul((vv[h >> 1] >> sh) & 0xFFFFu, (pw[h >> 1] >> sh) & 0xFFFFu);
+                vv[h >> 1] = (vv[h >> 1] & ~(0xFFFFu << sh)) | (y << sh);
+              }
+              eb_done = true;
+            }
+          }
           uint32_t lg[8];
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
+          for (int h = 0; h < 8 && !eb_done; ++h) {
             const uint32_t x = (vv[h >> 1] >> (16 * (h & 1))) & 0xFFFFu;
             lg[h] = (((eb >> h) & 1u) && x) ? uint32_t(__ldg(io.log_tab + x)) : 0u;
           }
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
+          for (int h = 0; h < 8 && !eb_done; ++h) {
             if (!((eb >> h) & 1u)) continue;
             const uint32_t sh = 16 * (h & 1);
             const uint32_t x = (vv[h >> 1] >> sh) & 0xFFFFu;
@@ -402,8 +415,17 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
             v = io.pkt ? io.merge_src[((b / io.pkt) * io.merge_stride + pos) * io.pkt + b % io.pkt]
                        : io.merge_src[b * io.merge_stride + pos];
           } else if (io.pinv_log && v) {
-            uint32_t t = uint32_t(io.log_tab[v]) + io.pinv_log[b * io.pinv_stride + pos];
-            v = io.exp_tab[t >= io.mord ? t - io.mord : t];
+            bool done = false;
+            if constexpr (R == 16) {
+              if (io.pinv_val) {
+                v = uint16_t(gf16_mul(v, io.pinv_log[b * io.pinv_stride + pos]));
+                done = true;
+              }
+            }
+            if (!done) {
+              uint32_t t = uint32_t(io.log_tab[v]) + io.pinv_log[b * io.pinv_stride + pos];
+              v = io.exp_tab[t >= io.mord ? t - io.mord : t];
+            }
           }
         }
         *const_cast<uint16_t *>(raw_addr(io, b, pos)) = v;
@@ -1060,20 +1082,14 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
       const uint4 *rxv = reinterpret_cast<const uint4 *>(p.rx + vec * p.rx_stride + j0);
       const uint4 r0 = __ldcs(rxv), r1 = __ldcs(rxv + 1);
       const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-      // phi = rx * Pi-bar through log/exp: all 16 log gathers, then all 16
-      // exp gathers, so each thread keeps 16 independent loads in flight
-      uint32_t lr[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const uint32_t r = (rw[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-        lr[e] = r ? uint32_t(__ldg(p.log + r)) : 0u;
-      }
+      // one independent exp gather per position: Pi-bar = alpha^v on survivors
+      // (phi = rx * Pi-bar by the table-free multiply), 1 / Pi' = alpha^-v on
+      // erasures (stored as values for the output epilogue)
       uint32_t ex[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        uint32_t t = lr[e] + v[e];
-        t = t >= M ? t - M : t;
-        ex[e] = __ldg(p.exp + t);
+        const bool erased = (er >> e) & 1u;
+        ex[e] = __ldg(p.exp + (erased ? (v[e] ? M - v[e] : 0u) : v[e]));
       }
       uint32_t o[8];
 #pragma unroll
@@ -1083,8 +1099,7 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
         for (int q = 0; q < 2; ++q) {
           const int e = 2 * h + q;
           const uint32_t r = (rw[h] >> (16 * q)) & 0xFFFFu;
-          const bool keep = !((er >> e) & 1u) && r;
-          pair |= (keep ? ex[e] : 0u) << (16 * q);
+          pair |= (((er >> e) & 1u) ? 0u : gf16_mul(r, ex[e])) << (16 * q);
         }
         o[h] = pair;
       }
@@ -1095,7 +1110,7 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
         uint16_t *pl = p.pinv_log + vec * p.k;
         uint32_t pv[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) pv[e] = ((er >> e) & 1u) ? (v[e] ? M - v[e] : 0u) : 0u;
+        for (int e = 0; e < 16; ++e) pv[e] = ((er >> e) & 1u) ? ex[e] : 0u;
         if (j0 + 16 <= p.k && (p.k & 7) == 0) {
           uint4 *pd = reinterpret_cast<uint4 *>(pl + j0);
           pd[0] = make_uint4(pv[0] | (pv[1] << 16), pv[2] | (pv[3] << 16), pv[4] | (pv[5] << 16),

@@ -66,6 +66,7 @@ struct RawIO {
   int64_t bits_stride;      // words between consecutive rows' bitmasks (0 = shared)
   const uint16_t *pinv_log; // [batch][pinv_stride] or null
   int64_t pinv_stride;
+  int pinv_val;             // R = 16: pinv_log holds alpha^pinv (values), multiplied without tables
   const uint16_t *log_tab, *exp_tab;
   uint32_t mord;            // 2^r - 1
   int vec;  // 16-byte vector accesses allowed

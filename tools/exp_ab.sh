@@ -1,4 +1,4 @@
-# parity + headline timing + gather launch durations
+# parity + config-4b timing + per-launch durations of the per-codeword decode
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 200 python bench.py --no-cpu --no-e2e --steps 10 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value'], d['encode_ms'], d['decode_ms'])"
-timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:"gather" -c 2 --csv python bench.py --no-cpu --no-e2e --steps 1 --warmup 1 --only decode 2>/dev/null | grep -E "gpu__time|dram__bytes" | awk -F'","' '{printf "%s %s | ", $(NF-2), $NF} END {print ""}'
+timeout 300 python bench.py --workload pcw --no-cpu --steps 5 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('pcw', d['value'], d['ms_per_step'])"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"locator16|pass_kernel|gather" --csv python bench.py --workload pcw --no-cpu --steps 1 --warmup 0 2>/dev/null | grep gpu__time | awk -F'","' '{printf "%s ", $NF} END {print ""}'

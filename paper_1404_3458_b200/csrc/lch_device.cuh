@@ -432,24 +432,34 @@ struct GF {
 };
 
 // Product of two GF(2^16) symbols (polynomial basis, x^16 + x^12 + x^3 + x + 1,
-// field.py:100-129) without tables: a carry-less 16x16 multiply from 16
-// integer multiplies of bit-interleaved quarters (bits of a and b spaced 4
-// apart, so every partial coefficient stays below 16 and a product's parity
-// bits never collide), then four folds of the high half by the taps.
-__device__ __forceinline__ uint32_t gf16_mul(uint32_t a, uint32_t b) {
-  const uint32_t a0 = a & 0x1111u, a1 = a & 0x2222u, a2 = a & 0x4444u, a3 = a & 0x8888u;
-  const uint32_t b0 = b & 0x1111u, b1 = b & 0x2222u, b2 = b & 0x4444u, b3 = b & 0x8888u;
-  const uint32_t z0 = (a0 * b0) ^ (a1 * b3) ^ (a2 * b2) ^ (a3 * b1);
-  const uint32_t z1 = (a0 * b1) ^ (a1 * b0) ^ (a2 * b3) ^ (a3 * b2);
-  const uint32_t z2 = (a0 * b2) ^ (a1 * b1) ^ (a2 * b0) ^ (a3 * b3);
-  const uint32_t z3 = (a0 * b3) ^ (a1 * b2) ^ (a2 * b1) ^ (a3 * b0);
-  uint32_t z = (z0 & 0x11111111u) | (z1 & 0x22222222u) | (z2 & 0x44444444u) | (z3 & 0x88888888u);
+// field.py:100-129) without tables.  gf16_clmul: the carry-less 16x16
+// product from 9 integer multiplies of bit-interleaved thirds (the bits of a
+// and b spaced 3 apart, so a partial coefficient is at most 6 < 8 and the
+// parity bits of one residue class never collide); gf16_fold: reduction by
+// the taps in four folds of the high half (or two byte-table lookups where a
+// kernel keeps gf16_red tables in shared memory).
+__device__ __forceinline__ uint32_t gf16_clmul(uint32_t a, uint32_t b) {
+  const uint32_t a0 = a & 0x9249u, a1 = a & 0x2492u, a2 = a & 0x4924u;
+  const uint32_t b0 = b & 0x9249u, b1 = b & 0x2492u, b2 = b & 0x4924u;
+  const uint32_t z0 = (a0 * b0) ^ (a1 * b2) ^ (a2 * b1);
+  const uint32_t z1 = (a0 * b1) ^ (a1 * b0) ^ (a2 * b2);
+  const uint32_t z2 = (a0 * b2) ^ (a1 * b1) ^ (a2 * b0);
+  return (z0 & 0x49249249u) | (z1 & 0x92492492u) | (z2 & 0x24924924u);
+}
+__host__ __device__ __forceinline__ uint32_t gf16_fold(uint32_t z) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {  // degree 30 -> 26 -> 22 -> 18 -> 14
     const uint32_t h = z >> 16;
     z = (z & 0xFFFFu) ^ h ^ (h << 1) ^ (h << 3) ^ (h << 12);
   }
   return z;
+}
+__device__ __forceinline__ uint32_t gf16_mul(uint32_t a, uint32_t b) { return gf16_fold(gf16_clmul(a, b)); }
+// gf16_red: red[x] = (x << 16) mod p for x < 256, red[256 + x] = (x << 24) mod p
+// for x < 128, so clmul(a, b) mod p = low ^ red[byte 2] ^ red[256 + byte 3].
+__device__ __forceinline__ uint32_t gf16_mul_t(uint32_t a, uint32_t b, const uint32_t *red) {
+  const uint32_t z = gf16_clmul(a, b);
+  return (z & 0xFFFFu) ^ red[(z >> 16) & 0xFFu] ^ red[256 + (z >> 24)];
 }
 
 // 32x32 bit-matrix transpose in registers: bit c of a[r] <-> bit r of a[c].

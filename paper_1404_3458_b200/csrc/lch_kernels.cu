@@ -978,6 +978,7 @@ __global__ void fwht_kernel(const __grid_constant__ FwhtParams p) {
 // indicator straight from the bitmask; the last writes the epilogue (locator
 // values / logs, or phi = rx * Pi_bar and -log Pi' for the decode).
 constexpr int LOC_NT = 1024;
+constexpr int LOC_SMEM = 65536 * 2 + 384 * 4;  // residues + gf16_red tables
 
 // x mod (2^16 - 1) folded once: (x & 0xFFFF) + (x >> 16) = x - 65535 * (x >> 16)
 // (shift + IMAD: keeps half of the work off the integer ALU pipe)
@@ -1008,12 +1009,14 @@ __device__ __forceinline__ void wht16(uint32_t (&v)[16]) {
 __device__ __forceinline__ uint32_t lsw(uint32_t w) { return w ^ (((w >> 7) & 3u) << 3); }
 
 __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant__ FwhtParams p) {
-  extern __shared__ uint16_t sv[];  // 2^16 residues
+  extern __shared__ uint16_t sv[];  // 2^16 residues, then the gf16_red tables
   uint32_t *const sw = reinterpret_cast<uint32_t *>(sv);
+  uint32_t *const red = sw + 32768;
   constexpr uint32_t M = 0xFFFFu;
   const int64_t vec = blockIdx.x;
   const uint32_t *bits = p.bits + vec * 2048;
   const int tid = threadIdx.x;
+  if (tid < 384) red[tid] = gf16_fold(tid < 256 ? uint32_t(tid) << 16 : uint32_t(tid - 256) << 24);
   // G0 of the first transform, from the bitmask (16 bits per slot), stored as
   // two 16-byte vectors per slot
   for (int slot = tid; slot < 4096; slot += LOC_NT) {
@@ -1099,7 +1102,7 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
         for (int q = 0; q < 2; ++q) {
           const int e = 2 * h + q;
           const uint32_t r = (rw[h] >> (16 * q)) & 0xFFFFu;
-          pair |= (((er >> e) & 1u) ? 0u : gf16_mul(r, ex[e])) << (16 * q);
+          pair |= (((er >> e) & 1u) ? 0u : gf16_mul_t(r, ex[e], red)) << (16 * q);
         }
         o[h] = pair;
       }
@@ -1160,9 +1163,9 @@ static int sm_count() {
 
 cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s) {
   static std::atomic<uint64_t> done{0};
-  cudaError_t e = smem_optin(locator16_kernel, 65536 * 2, done);
+  cudaError_t e = smem_optin(locator16_kernel, LOC_SMEM, done);
   if (e != cudaSuccess) return e;
-  locator16_kernel<<<unsigned(p.nvec), LOC_NT, 65536 * 2, s>>>(p);
+  locator16_kernel<<<unsigned(p.nvec), LOC_NT, LOC_SMEM, s>>>(p);
   return cudaGetLastError();
 }
 

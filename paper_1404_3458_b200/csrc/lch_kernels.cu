@@ -11,6 +11,7 @@
 // copies, laid out exactly like the shared-memory tile).
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "lch_device.cuh"
 #include "lch_kernels.h"
@@ -169,10 +170,10 @@ __device__ __forceinline__ const uint16_t *raw_addr(const RawIO &io, int64_t b, 
 
 // Issue the loads of a tile: BS input asynchronously (TMA bulk copies, see
 // below), raw input synchronously through registers into the staging layout.
-template <int R>
+template <int R, bool LEAN>
 __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, const uint32_t *tpos,
                                            int g, uint32_t base, int TP, uint64_t *bar) {
-  if (p.in_mode == IO_BS) {
+  if (LEAN || p.in_mode == IO_BS) {
     // lane 0 of every warp issues the blocks q = warp, warp + 8, ...; thread 0
     // supplies the barrier's single arrival
     if ((threadIdx.x & 31) == 0) {
@@ -543,7 +544,10 @@ struct FactorLoader {
   }
 };
 
-template <int R, uint32_t POLY>
+// LEAN: BS input and output, no per-position scalings, no gather epilogue
+// (the pure butterfly passes); the raw-I/O, scaling and gather code is
+// compiled out of that instance, which keeps its hot loop's code footprint small.
+template <int R, uint32_t POLY, bool LEAN>
 __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
@@ -585,14 +589,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  issue_tile<R>(p, smem, tpos, g, base, TP, &bar);
+  issue_tile<R, LEAN>(p, smem, tpos, g, base, TP, &bar);
   int fb = 0;  // factor-table buffer of the current tile
   {
     FactorLoader fl;
     fl.fetch(p, tpos, base);
     fl.put(fac[0]);
   }
-  if (p.in_mode == IO_BS) {
+  if (LEAN || p.in_mode == IO_BS) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
   }
@@ -601,16 +605,16 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // The last round keeps its data in registers and stores it straight to the
   // BS output, so the next tile's loads can stream into shared memory while
   // it computes.
-  const bool reg_path = p.nrounds > 0 && p.npost == 0 && p.out_mode == IO_BS && !p.gt_out;
+  const bool reg_path = p.nrounds > 0 && (LEAN || (p.npost == 0 && p.out_mode == IO_BS && !p.gt_out));
 
   for (;;) {
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
-    if (p.in_mode == IO_RAW) {
+    if (!LEAN && p.in_mode == IO_RAW) {
       if (!(p.dbg & 128)) finish_tile_raw<R>(smem, TP);
       __syncthreads();
     }
-    if (p.npre) {
+    if (!LEAN && p.npre) {
       scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
       __syncthreads();
     }
@@ -636,7 +640,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         __syncthreads();
         if (has_next) {
           const uint32_t nb = base_of(next);
-          issue_tile<R>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+          issue_tile<R, LEAN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
           if (!(p.dbg & 64)) nfl.fetch(p, tpos, nb);
         }
       }
@@ -754,11 +758,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (!last_reg) __syncthreads();
     }
     if (!reg_path) {
-      if (p.npost) {
+      if (!LEAN && p.npost) {
         scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
         __syncthreads();
       }
-      if (p.gt_out) {
+      if (!LEAN && p.gt_out) {
         // derivative gather over the tile bits (derivative.py:60-70), for the
         // output positions below 2^gt_lgH
         uint4 *gdst = p.gt_out + ((size_t(g) << p.gt_lgH) * U4);
@@ -778,14 +782,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           Blk<R>::store(gdst + size_t(pos) * U4, lane, acc);
         }
       }
-      if (p.out_mode == IO_BS)
+      if (LEAN || p.out_mode == IO_BS)
         store_tile_bs<R>(p, bsm, tpos, g, base, TP);
       else
         store_tile_raw<R>(p, smem, g, base, TP);
       __syncthreads();
       if (has_next) {
         const uint32_t nb = base_of(next);
-        issue_tile<R>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+        issue_tile<R, LEAN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
         FactorLoader fl;
         if (!(p.dbg & 64)) {
           fl.fetch(p, tpos, nb);
@@ -797,7 +801,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (lane == 0) tma_store_wait_all();
       break;
     }
-    if (p.in_mode == IO_BS) {
+    if (LEAN || p.in_mode == IO_BS) {
       mbar_wait(&bar, phase);
       phase ^= 1u;
     }
@@ -1262,13 +1266,18 @@ template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   const bool raw = p.in_mode == IO_RAW || p.out_mode == IO_RAW;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
-  static std::atomic<uint64_t> done{0};
-  cudaError_t e = smem_optin(pass_kernel<R, POLY>, int(pass_smem_bytes(R, TPB_MAX, true)), done);
+  const bool lean = !raw && p.npre == 0 && p.npost == 0 && !p.gt_out && !std::getenv("LCH_NO_LEAN");
+  static std::atomic<uint64_t> done{0}, done_lean{0};
+  cudaError_t e = lean ? smem_optin(pass_kernel<R, POLY, true>, int(pass_smem_bytes(R, TPB_MAX, true)), done_lean)
+                       : smem_optin(pass_kernel<R, POLY, false>, int(pass_smem_bytes(R, TPB_MAX, true)), done);
   if (e != cudaSuccess) return e;
   const int nsm = sm_count();
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
   const int64_t ctas = std::min<int64_t>(total, int64_t(2) * nsm);
-  pass_kernel<R, POLY><<<unsigned(ctas), NT, smem, s>>>(p);
+  if (lean)
+    pass_kernel<R, POLY, true><<<unsigned(ctas), NT, smem, s>>>(p);
+  else
+    pass_kernel<R, POLY, false><<<unsigned(ctas), NT, smem, s>>>(p);
   return cudaGetLastError();
 }
 

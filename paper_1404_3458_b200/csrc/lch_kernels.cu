@@ -170,10 +170,10 @@ __device__ __forceinline__ const uint16_t *raw_addr(const RawIO &io, int64_t b, 
 
 // Issue the loads of a tile: BS input asynchronously (TMA bulk copies, see
 // below), raw input synchronously through registers into the staging layout.
-template <int R, bool LEAN>
+template <int R, bool BS_ONLY>
 __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, const uint32_t *tpos,
                                            int g, uint32_t base, int TP, uint64_t *bar) {
-  if (LEAN || p.in_mode == IO_BS) {
+  if (BS_ONLY || p.in_mode == IO_BS) {
     // lane 0 of every warp issues the blocks q = warp, warp + 8, ...; thread 0
     // supplies the barrier's single arrival
     if ((threadIdx.x & 31) == 0) {
@@ -544,11 +544,13 @@ struct FactorLoader {
   }
 };
 
-// LEAN: BS input and output, no per-position scalings, no gather epilogue
-// (the pure butterfly passes); the raw-I/O, scaling and gather code is
-// compiled out of that instance, which keeps its hot loop's code footprint small.
-template <int R, uint32_t POLY, bool LEAN>
+// Instances by the features a pass needs (V bit 0: raw input/output, bit 1:
+// per-position scalings / gather epilogue); code a pass cannot reach is
+// compiled out, which keeps the hot loop's code footprint small (the pure
+// butterfly passes run 5-7 % faster in the V = 0 instance).
+template <int R, uint32_t POLY, int V>
 __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
+  constexpr bool RAW = V & 1, EXTRA = V & 2;
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
   uint4 *const bsm = smem + bs_offset_u4<R>();
@@ -589,14 +591,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  issue_tile<R, LEAN>(p, smem, tpos, g, base, TP, &bar);
+  issue_tile<R, !RAW>(p, smem, tpos, g, base, TP, &bar);
   int fb = 0;  // factor-table buffer of the current tile
   {
     FactorLoader fl;
     fl.fetch(p, tpos, base);
     fl.put(fac[0]);
   }
-  if (LEAN || p.in_mode == IO_BS) {
+  if (!RAW || p.in_mode == IO_BS) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
   }
@@ -605,16 +607,17 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // The last round keeps its data in registers and stores it straight to the
   // BS output, so the next tile's loads can stream into shared memory while
   // it computes.
-  const bool reg_path = p.nrounds > 0 && (LEAN || (p.npost == 0 && p.out_mode == IO_BS && !p.gt_out));
+  const bool reg_path = p.nrounds > 0 && (!EXTRA || (p.npost == 0 && !p.gt_out)) &&
+                        (!RAW || p.out_mode == IO_BS);
 
   for (;;) {
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
-    if (!LEAN && p.in_mode == IO_RAW) {
+    if (RAW && p.in_mode == IO_RAW) {
       if (!(p.dbg & 128)) finish_tile_raw<R>(smem, TP);
       __syncthreads();
     }
-    if (!LEAN && p.npre) {
+    if (EXTRA && p.npre) {
       scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
       __syncthreads();
     }
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         __syncthreads();
         if (has_next) {
           const uint32_t nb = base_of(next);
-          issue_tile<R, LEAN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+          issue_tile<R, !RAW>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
           if (!(p.dbg & 64)) nfl.fetch(p, tpos, nb);
         }
       }
@@ -758,11 +761,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (!last_reg) __syncthreads();
     }
     if (!reg_path) {
-      if (!LEAN && p.npost) {
+      if (EXTRA && p.npost) {
         scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
         __syncthreads();
       }
-      if (!LEAN && p.gt_out) {
+      if (EXTRA && p.gt_out) {
         // derivative gather over the tile bits (derivative.py:60-70), for the
         // output positions below 2^gt_lgH
         uint4 *gdst = p.gt_out + ((size_t(g) << p.gt_lgH) * U4);
@@ -782,14 +785,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           Blk<R>::store(gdst + size_t(pos) * U4, lane, acc);
         }
       }
-      if (LEAN || p.out_mode == IO_BS)
+      if (!RAW || p.out_mode == IO_BS)
         store_tile_bs<R>(p, bsm, tpos, g, base, TP);
       else
         store_tile_raw<R>(p, smem, g, base, TP);
       __syncthreads();
       if (has_next) {
         const uint32_t nb = base_of(next);
-        issue_tile<R, LEAN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+        issue_tile<R, !RAW>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
         FactorLoader fl;
         if (!(p.dbg & 64)) {
           fl.fetch(p, tpos, nb);
@@ -801,7 +804,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (lane == 0) tma_store_wait_all();
       break;
     }
-    if (LEAN || p.in_mode == IO_BS) {
+    if (!RAW || p.in_mode == IO_BS) {
       mbar_wait(&bar, phase);
       phase ^= 1u;
     }
@@ -812,6 +815,57 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     base = base_of(tl);
   }
 }
+
+// The dynamic shared-memory opt-in is a per-device function attribute: set it
+// once per (kernel, device) — a process may drive several GPUs.
+template <class K>
+static cudaError_t smem_optin(K *kernel, int bytes, std::atomic<uint64_t> &done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+static int sm_count() {
+  int dev = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) {
+    cudaGetLastError();
+    nsm = 148;
+  }
+  return nsm;
+}
+
+
+// One pass_kernel instance and its launch.  The instances are compiled in
+// separate translation units (this file built with -DLCH_PASS_TU=V, in
+// parallel), the main unit only declares them.
+template <int R, uint32_t POLY, int V>
+cudaError_t launch_pass_v(const PassParams &p, unsigned ctas, size_t smem, cudaStream_t s) {
+  static std::atomic<uint64_t> done{0};
+  cudaError_t e = smem_optin(pass_kernel<R, POLY, V>, int(pass_smem_bytes(R, TPB_MAX, true)), done);
+  if (e != cudaSuccess) return e;
+  pass_kernel<R, POLY, V><<<ctas, NT, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+#ifdef LCH_PASS_TU
+#if LCH_PASS_TU == 0 || LCH_PASS_TU == 3
+template cudaError_t launch_pass_v<8, 0x11Du, LCH_PASS_TU>(const PassParams &, unsigned, size_t, cudaStream_t);
+#endif
+template cudaError_t launch_pass_v<16, 0x1100Bu, LCH_PASS_TU>(const PassParams &, unsigned, size_t,
+                                                                cudaStream_t);
+#else  // the main unit: every kernel but the pass instances
+extern template cudaError_t launch_pass_v<8, 0x11Du, 0>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<8, 0x11Du, 3>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 0>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 1>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 2>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 3>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1141,30 +1195,6 @@ __global__ void __launch_bounds__(LOC_NT) locator16_kernel(const __grid_constant
   }
 }
 
-// The dynamic shared-memory opt-in is a per-device function attribute: set it
-// once per (kernel, device) — a process may drive several GPUs.
-template <class K>
-static cudaError_t smem_optin(K *kernel, int bytes, std::atomic<uint64_t> &done) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  const uint64_t bit = uint64_t(1) << (dev & 63);
-  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
-  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
-  return e;
-}
-
-static int sm_count() {
-  int dev = 0, nsm = 0;
-  cudaGetDevice(&dev);
-  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) {
-    cudaGetLastError();
-    nsm = 148;
-  }
-  return nsm;
-}
-
 cudaError_t launch_locator16(const FwhtParams &p, cudaStream_t s) {
   static std::atomic<uint64_t> done{0};
   cudaError_t e = smem_optin(locator16_kernel, LOC_SMEM, done);
@@ -1265,20 +1295,23 @@ size_t pass_smem_bytes(int R, int tpb, bool raw) {
 template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   const bool raw = p.in_mode == IO_RAW || p.out_mode == IO_RAW;
+  const bool extra = p.npre || p.npost || p.gt_out;
+  int v = (raw ? 1 : 0) | (extra ? 2 : 0);
+  if (R == 8 && v) v = 3;  // r = 8: the lean and the generic instance only
+  if (std::getenv("LCH_NO_LEAN")) v = 3;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
-  const bool lean = !raw && p.npre == 0 && p.npost == 0 && !p.gt_out && !std::getenv("LCH_NO_LEAN");
-  static std::atomic<uint64_t> done{0}, done_lean{0};
-  cudaError_t e = lean ? smem_optin(pass_kernel<R, POLY, true>, int(pass_smem_bytes(R, TPB_MAX, true)), done_lean)
-                       : smem_optin(pass_kernel<R, POLY, false>, int(pass_smem_bytes(R, TPB_MAX, true)), done);
-  if (e != cudaSuccess) return e;
-  const int nsm = sm_count();
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
-  const int64_t ctas = std::min<int64_t>(total, int64_t(2) * nsm);
-  if (lean)
-    pass_kernel<R, POLY, true><<<unsigned(ctas), NT, smem, s>>>(p);
-  else
-    pass_kernel<R, POLY, false><<<unsigned(ctas), NT, smem, s>>>(p);
-  return cudaGetLastError();
+  const unsigned ctas = unsigned(std::min<int64_t>(total, int64_t(2) * sm_count()));
+  if constexpr (R == 16) {
+    switch (v) {
+      case 0: return launch_pass_v<R, POLY, 0>(p, ctas, smem, s);
+      case 1: return launch_pass_v<R, POLY, 1>(p, ctas, smem, s);
+      case 2: return launch_pass_v<R, POLY, 2>(p, ctas, smem, s);
+      default: return launch_pass_v<R, POLY, 3>(p, ctas, smem, s);
+    }
+  } else {
+    return v == 0 ? launch_pass_v<R, POLY, 0>(p, ctas, smem, s) : launch_pass_v<R, POLY, 3>(p, ctas, smem, s);
+  }
 }
 
 template <int R, uint32_t POLY>
@@ -1510,5 +1543,6 @@ template cudaError_t launch_pass<16, 0x1100Bu>(const PassParams &, int, cudaStre
 template cudaError_t launch_pass<8, 0x11Du>(const PassParams &, int, cudaStream_t);
 template cudaError_t launch_gather<16, 0x1100Bu>(const GatherParams &, int, cudaStream_t);
 template cudaError_t launch_gather<8, 0x11Du>(const GatherParams &, int, cudaStream_t);
+#endif  // LCH_PASS_TU
 
 }  // namespace lch

@@ -544,13 +544,13 @@ struct FactorLoader {
   }
 };
 
-// Instances by the features a pass needs (V bit 0: raw input/output, bit 1:
-// per-position scalings / gather epilogue); code a pass cannot reach is
+// Instances by the features a pass needs (V bit 0: raw input, bit 1: raw
+// output, bit 2: per-position scalings / gather epilogue); code a pass cannot reach is
 // compiled out, which keeps the hot loop's code footprint small (the pure
 // butterfly passes run 5-7 % faster in the V = 0 instance).
 template <int R, uint32_t POLY, int V>
 __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
-  constexpr bool RAW = V & 1, EXTRA = V & 2;
+  constexpr bool RIN = V & 1, ROUT = V & 2, EXTRA = V & 4;
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
   uint4 *const bsm = smem + bs_offset_u4<R>();
@@ -591,14 +591,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  issue_tile<R, !RAW>(p, smem, tpos, g, base, TP, &bar);
+  issue_tile<R, !RIN>(p, smem, tpos, g, base, TP, &bar);
   int fb = 0;  // factor-table buffer of the current tile
   {
     FactorLoader fl;
     fl.fetch(p, tpos, base);
     fl.put(fac[0]);
   }
-  if (!RAW || p.in_mode == IO_BS) {
+  if (!RIN || p.in_mode == IO_BS) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
   }
@@ -608,12 +608,12 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // BS output, so the next tile's loads can stream into shared memory while
   // it computes.
   const bool reg_path = p.nrounds > 0 && (!EXTRA || (p.npost == 0 && !p.gt_out)) &&
-                        (!RAW || p.out_mode == IO_BS);
+                        (!ROUT || p.out_mode == IO_BS);
 
   for (;;) {
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
-    if (RAW && p.in_mode == IO_RAW) {
+    if (RIN && p.in_mode == IO_RAW) {
       if (!(p.dbg & 128)) finish_tile_raw<R>(smem, TP);
       __syncthreads();
     }
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         __syncthreads();
         if (has_next) {
           const uint32_t nb = base_of(next);
-          issue_tile<R, !RAW>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+          issue_tile<R, !RIN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
           if (!(p.dbg & 64)) nfl.fetch(p, tpos, nb);
         }
       }
@@ -785,14 +785,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           Blk<R>::store(gdst + size_t(pos) * U4, lane, acc);
         }
       }
-      if (!RAW || p.out_mode == IO_BS)
+      if (!ROUT || p.out_mode == IO_BS)
         store_tile_bs<R>(p, bsm, tpos, g, base, TP);
       else
         store_tile_raw<R>(p, smem, g, base, TP);
       __syncthreads();
       if (has_next) {
         const uint32_t nb = base_of(next);
-        issue_tile<R, !RAW>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+        issue_tile<R, !RIN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
         FactorLoader fl;
         if (!(p.dbg & 64)) {
           fl.fetch(p, tpos, nb);
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (lane == 0) tma_store_wait_all();
       break;
     }
-    if (!RAW || p.in_mode == IO_BS) {
+    if (!RIN || p.in_mode == IO_BS) {
       mbar_wait(&bar, phase);
       phase ^= 1u;
     }
@@ -854,18 +854,20 @@ cudaError_t launch_pass_v(const PassParams &p, unsigned ctas, size_t smem, cudaS
 }
 
 #ifdef LCH_PASS_TU
-#if LCH_PASS_TU == 0 || LCH_PASS_TU == 3
+#if LCH_PASS_TU == 0 || LCH_PASS_TU == 7
 template cudaError_t launch_pass_v<8, 0x11Du, LCH_PASS_TU>(const PassParams &, unsigned, size_t, cudaStream_t);
 #endif
 template cudaError_t launch_pass_v<16, 0x1100Bu, LCH_PASS_TU>(const PassParams &, unsigned, size_t,
                                                                 cudaStream_t);
 #else  // the main unit: every kernel but the pass instances
 extern template cudaError_t launch_pass_v<8, 0x11Du, 0>(const PassParams &, unsigned, size_t, cudaStream_t);
-extern template cudaError_t launch_pass_v<8, 0x11Du, 3>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<8, 0x11Du, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 0>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 1>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 2>(const PassParams &, unsigned, size_t, cudaStream_t);
-extern template cudaError_t launch_pass_v<16, 0x1100Bu, 3>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 4>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 5>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1295,22 +1297,23 @@ size_t pass_smem_bytes(int R, int tpb, bool raw) {
 template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   const bool raw = p.in_mode == IO_RAW || p.out_mode == IO_RAW;
-  const bool extra = p.npre || p.npost || p.gt_out;
-  int v = (raw ? 1 : 0) | (extra ? 2 : 0);
-  if (R == 8 && v) v = 3;  // r = 8: the lean and the generic instance only
-  if (std::getenv("LCH_NO_LEAN")) v = 3;
+  int v = (p.in_mode == IO_RAW ? 1 : 0) | (p.out_mode == IO_RAW ? 2 : 0) |
+          ((p.npre || p.npost || p.gt_out) ? 4 : 0);
+  if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
   const unsigned ctas = unsigned(std::min<int64_t>(total, int64_t(2) * sm_count()));
   if constexpr (R == 16) {
-    switch (v) {
+    switch (v) {  // the instances the codec's passes use; everything else runs generic
       case 0: return launch_pass_v<R, POLY, 0>(p, ctas, smem, s);
       case 1: return launch_pass_v<R, POLY, 1>(p, ctas, smem, s);
       case 2: return launch_pass_v<R, POLY, 2>(p, ctas, smem, s);
-      default: return launch_pass_v<R, POLY, 3>(p, ctas, smem, s);
+      case 4: return launch_pass_v<R, POLY, 4>(p, ctas, smem, s);
+      case 5: return launch_pass_v<R, POLY, 5>(p, ctas, smem, s);
+      default: return launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
     }
-  } else {
-    return v == 0 ? launch_pass_v<R, POLY, 0>(p, ctas, smem, s) : launch_pass_v<R, POLY, 3>(p, ctas, smem, s);
+  } else {  // r = 8: the lean and the generic instance only
+    return v == 0 ? launch_pass_v<R, POLY, 0>(p, ctas, smem, s) : launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
   }
 }
 

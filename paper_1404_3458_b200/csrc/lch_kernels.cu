@@ -16,6 +16,12 @@
 #include "lch_device.cuh"
 #include "lch_kernels.h"
 
+#ifdef LCH_PASS_DBG
+#define PDBG(x) (p.dbg & (x))  // LCH_DBG_PASS bisection flags (experiment builds only)
+#else
+#define PDBG(x) 0
+#endif
+
 namespace lch {
 
 namespace {
@@ -128,7 +134,7 @@ template <int R>
 __device__ __forceinline__ void store_tile_bs(const PassParams &p, const uint4 *smem,
                                               const uint32_t *tpos, int g, uint32_t base,
                                               int TP) {
-  if (p.dbg & 5) return;
+  if (PDBG(5)) return;
   constexpr int U4 = Blk<R>::U4;
   uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
   for (int idx = threadIdx.x; idx < TP * U4; idx += NT) {
@@ -182,7 +188,7 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
       const uint4 *src = p.bs_in + ((size_t(g) << p.lgH) * U4);
       const int w = threadIdx.x >> 5;
       fence_proxy_async();
-      if (!(p.dbg & 9)) {
+      if (!(PDBG(9))) {
         int nq = 0;
         for (int q = w; q < TP; q += NWARP) ++nq;
         if (nq) mbar_add_tx(bar, unsigned(nq * U4 * 16));
@@ -193,7 +199,7 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
     }
     return;
   }
-  if (p.dbg & 9) return;
+  if (PDBG(9)) return;
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
   const int WPR = TP >> 1;
   const int64_t row0 = int64_t(g) * GROUP;
@@ -287,7 +293,7 @@ __device__ __forceinline__ void column_to_words(const uint4 *bs, int cw, int lan
 template <int R>
 __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem, int g,
                                                uint32_t base, int TP) {
-  if (p.dbg & 5) return;
+  if (PDBG(5)) return;
   if (int64_t(base) + TP <= p.raw_out.pos_lo || int64_t(base) >= p.raw_out.pos_hi) return;
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
   const uint4 *bs = smem + bs_offset_u4<R>();
@@ -532,7 +538,7 @@ struct FactorLoader {
         const int qu = ((pp >> m) << (m + 1)) | (pp & ((1 << m) - 1));
         const int lvl = op.level;
         v[k] = uint32_t(__ldg(p.w_hat + p.w_hat_off[lvl] + ((base | tpos[qu]) >> (lvl + 1)))) ^ op.hs;
-        if (p.dbg & 256) v[k] = uint32_t(p.dbg) >> 16;  // experiment: one forced factor
+        if (PDBG(256)) v[k] = uint32_t(p.dbg) >> 16;  // experiment: one forced factor
         slot[k] = o * (1 << TPB_MAX) + qu;
       }
     }
@@ -545,12 +551,13 @@ struct FactorLoader {
 };
 
 // Instances by the features a pass needs (V bit 0: raw input, bit 1: raw
-// output, bit 2: per-position scalings / gather epilogue); code a pass cannot reach is
+// output, bit 2: per-position scalings / gather epilogue, bit 3: every round
+// is a straight-line one, so the general round path is left out); code a pass cannot reach is
 // compiled out, which keeps the hot loop's code footprint small (the pure
 // butterfly passes run 5-7 % faster in the V = 0 instance).
 template <int R, uint32_t POLY, int V>
 __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
-  constexpr bool RIN = V & 1, ROUT = V & 2, EXTRA = V & 4;
+  constexpr bool RIN = V & 1, ROUT = V & 2, EXTRA = V & 4, SHAPED = V & 8;
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
   uint4 *const bsm = smem + bs_offset_u4<R>();
@@ -614,7 +621,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
     if (RIN && p.in_mode == IO_RAW) {
-      if (!(p.dbg & 128)) finish_tile_raw<R>(smem, TP);
+      if (!(PDBG(128))) finish_tile_raw<R>(smem, TP);
       __syncthreads();
     }
     if (EXTRA && p.npre) {
@@ -630,7 +637,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       const bool active = warp < (1 << rr.nw);
       const int q0 = rr.q0w[warp];
       uint32_t a0[R], a1[R], a2[R], a3[R];
-      if (active && !(p.dbg & 32)) {
+      if (active && !(PDBG(32))) {
         Blk<R>::load(bsm + q0 * U4, lane, a0);
         Blk<R>::load(bsm + (q0 | M0) * U4, lane, a1);
         if (has1) {
@@ -644,10 +651,10 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         if (has_next) {
           const uint32_t nb = base_of(next);
           issue_tile<R, !RIN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
-          if (!(p.dbg & 64)) nfl.fetch(p, tpos, nb);
+          if (!(PDBG(64))) nfl.fetch(p, tpos, nb);
         }
       }
-      if (active && rr.shape != 0 && !(p.dbg & 2)) {
+      if (active && (SHAPED || rr.shape != 0) && !(PDBG(2))) {
         // straight-line rounds: [op along m0] or [op along m0, op along m1];
         // ops whose pairs share the factor run as one two-vector multiply
         const uint32_t *ft = fac[fb] + rr.op_begin * (1 << TPB_MAX);
@@ -672,18 +679,18 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
             butterfly<R, POLY>(a1, a3, fb2, ob.kind == OP_INV);
           }
         }
-        if (!last_reg && !(p.dbg & 32)) {
+        if (!last_reg && !(PDBG(32))) {
           Blk<R>::store(bsm + q0 * U4, lane, a0);
           Blk<R>::store(bsm + (q0 | M0) * U4, lane, a1);
           Blk<R>::store(bsm + (q0 | M1) * U4, lane, a2);
           Blk<R>::store(bsm + (q0 | M0 | M1) * U4, lane, a3);
         }
-      } else if (active) {
+      } else if (!SHAPED && active) {
         // A round's ops are [along m0]* [along m1]*.  Along m0 the pairs are
         // (a0,a1), (a2,a3); at the first m1 op a1 and a2 swap once, so the same
         // two inlined butterflies (one multiply body each) serve both bits.
         bool sw = false;
-        for (int o = rr.op_begin; o < ((p.dbg & 2) ? rr.op_begin : rr.op_end); ++o) {
+        for (int o = rr.op_begin; o < ((PDBG(2)) ? rr.op_begin : rr.op_end); ++o) {
           const PassOp &op = p.ops[o];
           const bool inv = op.kind == OP_INV;
           if (op.m == 1 && !sw) {
@@ -720,19 +727,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           }
         }
       }
-      if (last_reg && (p.dbg & 16)) {
-        // experiment: direct register -> global stores
-        if (active && !(p.dbg & 5)) {
-          uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
-          Blk<R>::store(dst + size_t(base | tpos[q0]) * U4, lane, a0);
-          Blk<R>::store(dst + size_t(base | tpos[q0 | M0]) * U4, lane, a1);
-          if (has1) {
-            Blk<R>::store(dst + size_t(base | tpos[q0 | M1]) * U4, lane, a2);
-            Blk<R>::store(dst + size_t(base | tpos[q0 | M0 | M1]) * U4, lane, a3);
-          }
-        }
-        if (has_next && !(p.dbg & 64)) nfl.put(fac[fb ^ 1]);
-      } else if (last_reg) {
+      if (last_reg) {
         // Drain the tile with bulk stores through a private 4 KB staging area
         // per warp (two positions at a time): only warp-level syncs, and the
         // stores overlap the next tile's rounds.
@@ -749,14 +744,14 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
             Blk<R>::store(stg + U4, lane, h ? a3 : a1);
             fence_proxy_async();
             __syncwarp();
-            if (lane == 0 && !(p.dbg & 5)) {
+            if (lane == 0 && !(PDBG(5))) {
               tma_store_1d(dst + size_t(base | tpos[qs[2 * h]]) * U4, stg, U4 * 16);
               tma_store_1d(dst + size_t(base | tpos[qs[2 * h + 1]]) * U4, stg + U4, U4 * 16);
               tma_store_commit();
             }
           }
         }
-        if (has_next && !(p.dbg & 64)) nfl.put(fac[fb ^ 1]);
+        if (has_next && !(PDBG(64))) nfl.put(fac[fb ^ 1]);
       }
       if (!last_reg) __syncthreads();
     }
@@ -794,7 +789,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         const uint32_t nb = base_of(next);
         issue_tile<R, !RIN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
         FactorLoader fl;
-        if (!(p.dbg & 64)) {
+        if (!(PDBG(64))) {
           fl.fetch(p, tpos, nb);
           fl.put(fac[fb ^ 1]);
         }
@@ -868,6 +863,9 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 2>(const PassParams &, u
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 4>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 5>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 8>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 9>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 10>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1299,6 +1297,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   const bool raw = p.in_mode == IO_RAW || p.out_mode == IO_RAW;
   int v = (p.in_mode == IO_RAW ? 1 : 0) | (p.out_mode == IO_RAW ? 2 : 0) |
           ((p.npre || p.npost || p.gt_out) ? 4 : 0);
+  bool shaped = p.nrounds > 0;
+  for (int r = 0; r < p.nrounds; ++r) shaped = shaped && p.rounds[r].shape != 0;
+  if (shaped && (v == 0 || v == 1 || v == 2)) v |= 8;
   if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
@@ -1310,10 +1311,13 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 2: return launch_pass_v<R, POLY, 2>(p, ctas, smem, s);
       case 4: return launch_pass_v<R, POLY, 4>(p, ctas, smem, s);
       case 5: return launch_pass_v<R, POLY, 5>(p, ctas, smem, s);
+      case 8: return launch_pass_v<R, POLY, 8>(p, ctas, smem, s);
+      case 9: return launch_pass_v<R, POLY, 9>(p, ctas, smem, s);
+      case 10: return launch_pass_v<R, POLY, 10>(p, ctas, smem, s);
       default: return launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
     }
   } else {  // r = 8: the lean and the generic instance only
-    return v == 0 ? launch_pass_v<R, POLY, 0>(p, ctas, smem, s) : launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
+    return (v & 7) == 0 ? launch_pass_v<R, POLY, 0>(p, ctas, smem, s) : launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
   }
 }
 

@@ -2,6 +2,7 @@
 
 LCH_DBG_PASS=1 skips global I/O in the pass kernel, =2 skips butterflies
 (results are then wrong; this only separates memory from compute time).
+The flags need a library built with `make EXTRA=-DLCH_PASS_DBG`.
 """
 import os
 import sys

@@ -558,6 +558,9 @@ struct FactorLoader {
 template <int R, uint32_t POLY, int V>
 __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
   constexpr bool RIN = V & 1, ROUT = V & 2, EXTRA = V & 4, SHAPED = V & 8;
+  // bits 4-5: every round follows one pattern -- 1: inverse (op along m0 with
+  // distinct factors, op along m1 shared), 2: forward (m0 shared, m1 distinct)
+  constexpr int PAT = (V >> 4) & 3;
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
   uint4 *const bsm = smem + bs_offset_u4<R>();
@@ -660,23 +663,25 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         const uint32_t *ft = fac[fb] + rr.op_begin * (1 << TPB_MAX);
         const PassOp &oa = p.ops[rr.op_begin];
         const uint32_t fa = __shfl_sync(0xffffffffu, ft[q0], 0);
-        if (oa.shared) {
-          butterfly2<R, POLY>(a0, a1, a2, a3, fa, oa.kind == OP_INV);
+        const bool inv_a = PAT ? PAT == 1 : oa.kind == OP_INV;
+        if (PAT ? PAT == 2 : oa.shared) {
+          butterfly2<R, POLY>(a0, a1, a2, a3, fa, inv_a);
         } else {
           const uint32_t fa2 = __shfl_sync(0xffffffffu, ft[q0 | M1], 0);
-          butterfly<R, POLY>(a0, a1, fa, oa.kind == OP_INV);
-          butterfly<R, POLY>(a2, a3, fa2, oa.kind == OP_INV);
+          butterfly<R, POLY>(a0, a1, fa, inv_a);
+          butterfly<R, POLY>(a2, a3, fa2, inv_a);
         }
         if (rr.shape == 2) {
           const uint32_t *fu = ft + (1 << TPB_MAX);
           const PassOp &ob = p.ops[rr.op_begin + 1];
           const uint32_t fb1 = __shfl_sync(0xffffffffu, fu[q0], 0);
-          if (ob.shared) {
-            butterfly2<R, POLY>(a0, a2, a1, a3, fb1, ob.kind == OP_INV);
+          const bool inv_b = PAT ? PAT == 1 : ob.kind == OP_INV;
+          if (PAT ? PAT == 1 : ob.shared) {
+            butterfly2<R, POLY>(a0, a2, a1, a3, fb1, inv_b);
           } else {
             const uint32_t fb2 = __shfl_sync(0xffffffffu, fu[q0 | M0], 0);
-            butterfly<R, POLY>(a0, a2, fb1, ob.kind == OP_INV);
-            butterfly<R, POLY>(a1, a3, fb2, ob.kind == OP_INV);
+            butterfly<R, POLY>(a0, a2, fb1, inv_b);
+            butterfly<R, POLY>(a1, a3, fb2, inv_b);
           }
         }
         if (!last_reg && !(PDBG(32))) {
@@ -866,6 +871,8 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 7>(const PassParams &, u
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 8>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 9>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 10>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 42>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1299,7 +1306,29 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
           ((p.npre || p.npost || p.gt_out) ? 4 : 0);
   bool shaped = p.nrounds > 0;
   for (int r = 0; r < p.nrounds; ++r) shaped = shaped && p.rounds[r].shape != 0;
-  if (shaped && (v == 0 || v == 1 || v == 2)) v |= 8;
+  if (shaped && (v == 0 || v == 1 || v == 2)) {
+    v |= 8;
+    // one butterfly pattern for every round (inverse- or forward-only passes)
+    for (int pat = 1; pat <= 2; ++pat) {
+      bool ok = true;
+      for (int r = 0; r < p.nrounds && ok; ++r) {
+        const PassRound &rr = p.rounds[r];
+        const PassOp &a = p.ops[rr.op_begin];
+        ok = a.kind == (pat == 1 ? OP_INV : OP_FWD) && (a.shared != 0) == (pat == 2);
+        if (ok && rr.shape == 2) {
+          const PassOp &b = p.ops[rr.op_begin + 1];
+          ok = b.kind == a.kind && (b.shared != 0) == (pat == 1);
+        }
+      }
+      const int vp = v | (pat << 4);
+      // the instantiated ones: forward-only passes (the inverse-pattern
+      // instances measured slower than the shaped ones and are not built)
+      if (ok && (vp == 40 || vp == 42)) {
+        v = vp;
+        break;
+      }
+    }
+  }
   if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
@@ -1314,6 +1343,8 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 8: return launch_pass_v<R, POLY, 8>(p, ctas, smem, s);
       case 9: return launch_pass_v<R, POLY, 9>(p, ctas, smem, s);
       case 10: return launch_pass_v<R, POLY, 10>(p, ctas, smem, s);
+      case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);
+      case 42: return launch_pass_v<R, POLY, 42>(p, ctas, smem, s);
       default: return launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
     }
   } else {  // r = 8: the lean and the generic instance only

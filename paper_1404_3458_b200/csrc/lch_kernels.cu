@@ -871,6 +871,9 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 7>(const PassParams &, u
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 8>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 9>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 10>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 12>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 42>(const PassParams &, unsigned, size_t, cudaStream_t);
 
@@ -1306,7 +1309,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
           ((p.npre || p.npost || p.gt_out) ? 4 : 0);
   bool shaped = p.nrounds > 0;
   for (int r = 0; r < p.nrounds; ++r) shaped = shaped && p.rounds[r].shape != 0;
-  if (shaped && (v == 0 || v == 1 || v == 2)) {
+  if (shaped && (v == 0 || v == 1 || v == 2 || v == 4 || v == 5)) {
     v |= 8;
     // one butterfly pattern for every round (inverse- or forward-only passes)
     for (int pat = 1; pat <= 2; ++pat) {
@@ -1323,7 +1326,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       const int vp = v | (pat << 4);
       // the instantiated ones: forward-only passes (the inverse-pattern
       // instances measured slower than the shaped ones and are not built)
-      if (ok && (vp == 40 || vp == 42)) {
+      if (ok && (vp == 40 || vp == 42 || vp == 44)) {
         v = vp;
         break;
       }
@@ -1343,6 +1346,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 8: return launch_pass_v<R, POLY, 8>(p, ctas, smem, s);
       case 9: return launch_pass_v<R, POLY, 9>(p, ctas, smem, s);
       case 10: return launch_pass_v<R, POLY, 10>(p, ctas, smem, s);
+      case 12: return launch_pass_v<R, POLY, 12>(p, ctas, smem, s);
+      case 13: return launch_pass_v<R, POLY, 13>(p, ctas, smem, s);
+      case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);
       case 42: return launch_pass_v<R, POLY, 42>(p, ctas, smem, s);
       default: return launch_pass_v<R, POLY, 7>(p, ctas, smem, s);

@@ -1,8 +1,6 @@
-# pass-instance A/B (LCH_NO_LEAN=1: generic instance everywhere) + full parity
+# parity + headline timing + per-launch durations of the headline step
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-for v in 0 1 0 1; do
-  if [ $v = 1 ]; then export LCH_NO_LEAN=1; else unset LCH_NO_LEAN; fi
-  timeout 200 python bench.py --no-cpu --no-e2e --steps 10 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('no_lean=$v', d['value'], d['encode_ms'], d['decode_ms'])"
+for v in 0 0; do
+  timeout 200 python bench.py --no-cpu --no-e2e --steps 10 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value'], d['encode_ms'], d['decode_ms'])"
 done
-unset LCH_NO_LEAN
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"pass_kernel|gather" --csv python bench.py --no-cpu --no-e2e --steps 1 --warmup 1 2>/dev/null | grep gpu__time | awk -F'","' '{printf "%s ", $NF} END {print ""}'

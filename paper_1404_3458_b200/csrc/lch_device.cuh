@@ -396,7 +396,7 @@ struct GF {
                                              uint32_t f) {
 #pragma unroll
     for (int b = 0; b < R; ++b) acc[b] = 0u;
-    mul_acc(acc, v, f);
+    mul_acc_n2(acc, v, f);
   }
 
   // acc = f_lane * v where the factor differs per lane (not warp-uniform):

@@ -459,7 +459,7 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
       uint32_t acc[R];
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] = 0u;
-      if (f) F::mul_acc_1(acc, v, f);
+      if (f) F::mul_acc_n2(acc, v, f);
 #pragma unroll
       for (int b = 0; b < R; ++b) v[b] = acc[b];
     }

@@ -1682,7 +1682,9 @@ int lch_pointwise_mul(lch_ctx *c, const uint16_t *a, const uint16_t *b, uint16_t
   LCH_TRY(ensure_device(c));
   if (count == 0) return LCH_OK;
   c->launches++;
-  return cu(launch_pointwise_mul(a, b, out, count, c->d_log, c->d_exp, c->t.m,
+  // r = 16 with the reference polynomial: the table-free product (gf16_mul)
+  const bool clmul = c->t.r == 16 && c->t.poly == 0x1100Bu;
+  return cu(launch_pointwise_mul(a, b, out, count, clmul ? nullptr : c->d_log, c->d_exp, c->t.m,
                                  static_cast<cudaStream_t>(stream)));
 }
 

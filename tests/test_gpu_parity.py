@@ -349,3 +349,31 @@ def test_poly_mul_vs_oracle(lch, bt8, bt16, orc8, orc16, r, h):
     np.testing.assert_array_equal(np.asarray(got, np.uint16), orc.inverse(prod, 0))
     if h == 1:
         assert lch.poly_mul(bt, lch.CoeffVec([1]), lch.CoeffVec([1])).data == [1, 0]  # test_transform.py:137-141
+
+
+@pytest.mark.parametrize("r", [8, 16])
+def test_pointwise_mul_vs_tables(lch, bt8, bt16, orc8, orc16, r):
+    """lch_pointwise_mul against the log/exp product of the oracle's tables
+    (field.py:100-129): r = 16 runs the table-free carry-less multiply
+    (gf16_mul, also used by the per-codeword decode), r = 8 the table path.
+    Random pairs plus every product of the edge symbols 0, 1, 2, top bit, all ones."""
+    import torch
+
+    from paper_1404_3458_b200 import _lib
+    bt, orc = (bt8, orc8) if r == 8 else (bt16, orc16)
+    t = orc.tables()
+    m = (1 << r) - 1
+    rng = np.random.default_rng(1404 + r)
+    a = rng.integers(0, 1 << r, 1 << 20).astype(np.uint16)
+    b = rng.integers(0, 1 << r, 1 << 20).astype(np.uint16)
+    edge = np.array([0, 1, 2, 1 << (r - 1), m, m - 1, 0x5A & m], np.uint16)
+    a = np.concatenate([a, np.repeat(edge, len(edge))])
+    b = np.concatenate([b, np.tile(edge, len(edge))])
+    lg, ex = t["log"].astype(np.int64), t["exp"].astype(np.int64)
+    want = np.where((a == 0) | (b == 0), 0, ex[(lg[a] + lg[b]) % m]).astype(np.uint16)
+    da, db = dev(a), dev(b)
+    out = torch.empty_like(da)
+    _lib.check(_lib.lib.lch_pointwise_mul(bt.ctx.handle, da.data_ptr(), db.data_ptr(), out.data_ptr(),
+                                          len(a), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(host(out), want)

@@ -7,6 +7,7 @@
 #include <immintrin.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -90,13 +91,51 @@ namespace {
 
 __attribute__((target("avx512f,avx512bw,avx512vbmi2"))) void compact_row_avx512(
     const uint16_t *src, const uint32_t *erased, int64_t n, uint16_t *dst) {
+  // Survivors are compressed in registers and collected into whole 64-byte
+  // lines that leave with non-temporal stores when dst is 64-byte aligned
+  // (the page-locked staging rows are): the lines are not read for ownership
+  // first, which saves host memory bandwidth the DMA engines share.
+  if (reinterpret_cast<uintptr_t>(dst) & 63) {
+    uint16_t *o = dst;
+    for (int64_t w = 0; w < n / 32; ++w) {
+      const __mmask32 keep = ~erased[w];
+      const __m512i v = _mm512_loadu_si512(reinterpret_cast<const void *>(src + 32 * w));
+      _mm512_mask_compressstoreu_epi16(o, keep, v);
+      o += __builtin_popcount(keep);
+    }
+    return;
+  }
+  // idx[j] = j for lanes below the pending count p, 32 + (j - p) above it:
+  // permutex2var(pend, idx, c) appends c behind the p pending symbols
+  const __m512i iota = _mm512_set_epi16(31, 30, 29, 28, 27, 26, 25, 24, 23, 22, 21, 20, 19, 18, 17, 16,
+                                        15, 14, 13, 12, 11, 10, 9, 8, 7, 6, 5, 4, 3, 2, 1, 0);
+  __m512i pend = _mm512_setzero_si512();
+  int np = 0;
   uint16_t *o = dst;
   for (int64_t w = 0; w < n / 32; ++w) {
     const __mmask32 keep = ~erased[w];
+    const int cnt = __builtin_popcount(keep);
     const __m512i v = _mm512_loadu_si512(reinterpret_cast<const void *>(src + 32 * w));
-    _mm512_mask_compressstoreu_epi16(o, keep, v);
-    o += __builtin_popcount(keep);
+    const __m512i c = _mm512_maskz_compress_epi16(keep, v);
+    const __m512i pv = _mm512_set1_epi16(short(np));
+    // lanes >= np take c[j - np] (index 32 + j - np selects the second table)
+    const __m512i idx = _mm512_mask_add_epi16(iota, _mm512_cmpge_epu16_mask(iota, pv), iota,
+                                              _mm512_sub_epi16(_mm512_set1_epi16(32), pv));
+    const __m512i merged = _mm512_permutex2var_epi16(pend, idx, c);
+    if (np + cnt >= 32) {
+      _mm512_stream_si512(reinterpret_cast<__m512i *>(o), merged);
+      o += 32;
+      // the rest of c (from index 32 - np) becomes the pending prefix
+      const int used = 32 - np;
+      pend = _mm512_permutexvar_epi16(_mm512_add_epi16(iota, _mm512_set1_epi16(short(used))), c);
+      np = cnt - used;
+    } else {
+      pend = merged;
+      np += cnt;
+    }
   }
+  if (np) _mm512_mask_storeu_epi16(o, __mmask32((1u << np) - 1u), pend);
+  _mm_sfence();
 }
 
 void compact_row_scalar(const uint16_t *src, const uint32_t *erased, int64_t n, uint16_t *dst) {

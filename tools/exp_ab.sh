@@ -1,4 +1,7 @@
-# full GPU suite + headline and config-4b timing
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 200 python bench.py --no-cpu --no-e2e --steps 10 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench', d['value'], d['encode_ms'], d['decode_ms'])"
-timeout 300 python bench.py --workload pcw --no-cpu --steps 5 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('pcw', d['value'], d['ms_per_step'])"
+# host compaction A/B: streaming-store compaction (_build) vs compress-store (_build_old)
+timeout 600 python -m pytest tests/test_gpu_host.py -x -q -m gpu 2>&1 | tail -2
+for rep in 1 2 3; do
+for so in paper_1404_3458_b200/_build/liblch.so paper_1404_3458_b200/_build_old/liblch.so; do
+  echo "$so $(LCH_SO_PATH=$so timeout 120 python tools/compact_bw.py 4096 2>&1 | tail -1) | $(LCH_SO_PATH=$so timeout 300 python tools/e2e_phases.py 2>&1 | grep -E 'decode_host:|both' | tr '\n' ' ')"
+done
+done

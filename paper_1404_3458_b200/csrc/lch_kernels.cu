@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         const uint32_t *ft = fac[fb] + rr.op_begin * (1 << TPB_MAX);
         const PassOp &oa = p.ops[rr.op_begin];
         const uint32_t fa = __shfl_sync(0xffffffffu, ft[q0], 0);
-        const bool inv_a = PAT ? PAT == 1 : oa.kind == OP_INV;
+        const bool inv_a = PAT == 2 ? false : oa.kind == OP_INV;
         if (PAT ? PAT == 2 : oa.shared) {
           butterfly2<R, POLY>(a0, a1, a2, a3, fa, inv_a);
         } else {
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           const uint32_t *fu = ft + (1 << TPB_MAX);
           const PassOp &ob = p.ops[rr.op_begin + 1];
           const uint32_t fb1 = __shfl_sync(0xffffffffu, fu[q0], 0);
-          const bool inv_b = PAT ? PAT == 1 : ob.kind == OP_INV;
+          const bool inv_b = PAT == 2 ? false : ob.kind == OP_INV;
           if (PAT ? PAT == 1 : ob.shared) {
             butterfly2<R, POLY>(a0, a2, a1, a3, fb1, inv_b);
           } else {
@@ -872,6 +872,7 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 8>(const PassParams &, u
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 9>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 10>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 12>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 24>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
@@ -1324,9 +1325,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
         }
       }
       const int vp = v | (pat << 4);
-      // the instantiated ones: forward-only passes (the inverse-pattern
-      // instances measured slower than the shaped ones and are not built)
-      if (ok && (vp == 40 || vp == 42 || vp == 44)) {
+      // the instantiated ones (inverse pattern: the op kinds stay runtime
+      // values there, a compile-time kind measured slower)
+      if (ok && (vp == 24 || vp == 40 || vp == 42 || vp == 44)) {
         v = vp;
         break;
       }
@@ -1347,6 +1348,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 9: return launch_pass_v<R, POLY, 9>(p, ctas, smem, s);
       case 10: return launch_pass_v<R, POLY, 10>(p, ctas, smem, s);
       case 12: return launch_pass_v<R, POLY, 12>(p, ctas, smem, s);
+      case 24: return launch_pass_v<R, POLY, 24>(p, ctas, smem, s);
       case 13: return launch_pass_v<R, POLY, 13>(p, ctas, smem, s);
       case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);

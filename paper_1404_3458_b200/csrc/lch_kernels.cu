@@ -873,6 +873,9 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 9>(const PassParams &, u
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 10>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 12>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 24>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 25>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 28>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 29>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
@@ -1327,7 +1330,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       const int vp = v | (pat << 4);
       // the instantiated ones (inverse pattern: the op kinds stay runtime
       // values there, a compile-time kind measured slower)
-      if (ok && (vp == 24 || vp == 40 || vp == 42 || vp == 44)) {
+      if (ok && (vp == 24 || vp == 25 || vp == 28 || vp == 29 || vp == 40 || vp == 42 || vp == 44)) {
         v = vp;
         break;
       }
@@ -1349,6 +1352,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 10: return launch_pass_v<R, POLY, 10>(p, ctas, smem, s);
       case 12: return launch_pass_v<R, POLY, 12>(p, ctas, smem, s);
       case 24: return launch_pass_v<R, POLY, 24>(p, ctas, smem, s);
+      case 25: return launch_pass_v<R, POLY, 25>(p, ctas, smem, s);
+      case 28: return launch_pass_v<R, POLY, 28>(p, ctas, smem, s);
+      case 29: return launch_pass_v<R, POLY, 29>(p, ctas, smem, s);
       case 13: return launch_pass_v<R, POLY, 13>(p, ctas, smem, s);
       case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);

@@ -876,6 +876,7 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 24>(const PassParams &, 
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 25>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 28>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 29>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 46>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
@@ -1313,7 +1314,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
           ((p.npre || p.npost || p.gt_out) ? 4 : 0);
   bool shaped = p.nrounds > 0;
   for (int r = 0; r < p.nrounds; ++r) shaped = shaped && p.rounds[r].shape != 0;
-  if (shaped && (v == 0 || v == 1 || v == 2 || v == 4 || v == 5)) {
+  if (shaped && v != 3 && v != 7) {
     v |= 8;
     // one butterfly pattern for every round (inverse- or forward-only passes)
     for (int pat = 1; pat <= 2; ++pat) {
@@ -1330,7 +1331,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       const int vp = v | (pat << 4);
       // the instantiated ones (inverse pattern: the op kinds stay runtime
       // values there, a compile-time kind measured slower)
-      if (ok && (vp == 24 || vp == 25 || vp == 28 || vp == 29 || vp == 40 || vp == 42 || vp == 44)) {
+      if (ok && (vp == 24 || vp == 25 || vp == 28 || vp == 29 || vp == 40 || vp == 42 || vp == 44 || vp == 46)) {
         v = vp;
         break;
       }
@@ -1355,6 +1356,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 25: return launch_pass_v<R, POLY, 25>(p, ctas, smem, s);
       case 28: return launch_pass_v<R, POLY, 28>(p, ctas, smem, s);
       case 29: return launch_pass_v<R, POLY, 29>(p, ctas, smem, s);
+      case 46: return launch_pass_v<R, POLY, 46>(p, ctas, smem, s);
       case 13: return launch_pass_v<R, POLY, 13>(p, ctas, smem, s);
       case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);

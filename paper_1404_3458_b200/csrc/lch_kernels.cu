@@ -176,7 +176,7 @@ __device__ __forceinline__ const uint16_t *raw_addr(const RawIO &io, int64_t b, 
 
 // Issue the loads of a tile: BS input asynchronously (TMA bulk copies, see
 // below), raw input synchronously through registers into the staging layout.
-template <int R, bool BS_ONLY>
+template <int R, bool BS_ONLY, bool ROWONLY = false>
 __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, const uint32_t *tpos,
                                            int g, uint32_t base, int TP, uint64_t *bar) {
   if (BS_ONLY || p.in_mode == IO_BS) {
@@ -209,7 +209,7 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
     // tile entirely outside the input window: zeros
     uint4 *z = smem;
     for (int idx = threadIdx.x; idx < WPR * (GROUP / 4); idx += NT) z[idx] = make_uint4(0u, 0u, 0u, 0u);
-  } else if (io.pkt && inwin) {
+  } else if (!ROWONLY && io.pkt && inwin) {
     // packet-major: 1024 consecutive symbols per position; a thread takes 8
     // rows of one word column (positions 2cw, 2cw+1) and interleaves them
     for (int idx = threadIdx.x; idx < WPR * (GROUP / 8); idx += NT) {
@@ -290,7 +290,7 @@ __device__ __forceinline__ void column_to_words(const uint4 *bs, int cw, int lan
   transpose32(a);
 }
 
-template <int R>
+template <int R, bool ROWONLY = false>
 __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem, int g,
                                                uint32_t base, int TP) {
   if (PDBG(5)) return;
@@ -314,7 +314,7 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
     const int64_t row = io.pkt ? b / io.pkt : b;
     return (io.merge_bits[row * io.bits_stride + (j >> 5)] >> (j & 31)) & 1u;
   };
-  if (io.pkt && inwin) {
+  if (!ROWONLY && io.pkt && inwin) {
     for (int idx = tid; idx < WPR * (GROUP / 8); idx += NT) {
       const int cw = idx / (GROUP / 8), r8 = idx - cw * (GROUP / 8);
       const uint4 *srcw = reinterpret_cast<const uint4 *>(rs + stage_idx(8 * r8, cw));
@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // bits 4-5: every round follows one pattern -- 1: inverse (op along m0 with
   // distinct factors, op along m1 shared), 2: forward (m0 shared, m1 distinct)
   constexpr int PAT = (V >> 4) & 3;
+  constexpr bool ROWONLY = V & 128;  // raw I/O in row layout only (no packet paths)
   constexpr int U4 = Blk<R>::U4;
   extern __shared__ uint4 smem[];
   uint4 *const bsm = smem + bs_offset_u4<R>();
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  issue_tile<R, !RIN>(p, smem, tpos, g, base, TP, &bar);
+  issue_tile<R, !RIN, ROWONLY>(p, smem, tpos, g, base, TP, &bar);
   int fb = 0;  // factor-table buffer of the current tile
   {
     FactorLoader fl;
@@ -653,7 +654,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         __syncthreads();
         if (has_next) {
           const uint32_t nb = base_of(next);
-          issue_tile<R, !RIN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+          issue_tile<R, !RIN, ROWONLY>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
           if (!(PDBG(64))) nfl.fetch(p, tpos, nb);
         }
       }
@@ -788,11 +789,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (!ROUT || p.out_mode == IO_BS)
         store_tile_bs<R>(p, bsm, tpos, g, base, TP);
       else
-        store_tile_raw<R>(p, smem, g, base, TP);
+        store_tile_raw<R, ROWONLY>(p, smem, g, base, TP);
       __syncthreads();
       if (has_next) {
         const uint32_t nb = base_of(next);
-        issue_tile<R, !RIN>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
+        issue_tile<R, !RIN, ROWONLY>(p, smem, tpos, next >> p.lgnt, nb, TP, &bar);
         FactorLoader fl;
         if (!(PDBG(64))) {
           fl.fetch(p, tpos, nb);
@@ -877,6 +878,10 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 25>(const PassParams &, 
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 28>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 29>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 46>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 153>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 157>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 170>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 174>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
@@ -1337,6 +1342,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       }
     }
   }
+  // row-layout raw I/O (no stripe packets): the packet code paths compiled out
+  const bool rows = (p.in_mode != IO_RAW || p.raw_in.pkt == 0) && (p.out_mode != IO_RAW || p.raw_out.pkt == 0);
+  if (rows && (v == 25 || v == 29 || v == 42 || v == 46)) v |= 128;
   if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
@@ -1357,6 +1365,10 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 28: return launch_pass_v<R, POLY, 28>(p, ctas, smem, s);
       case 29: return launch_pass_v<R, POLY, 29>(p, ctas, smem, s);
       case 46: return launch_pass_v<R, POLY, 46>(p, ctas, smem, s);
+      case 153: return launch_pass_v<R, POLY, 153>(p, ctas, smem, s);
+      case 157: return launch_pass_v<R, POLY, 157>(p, ctas, smem, s);
+      case 170: return launch_pass_v<R, POLY, 170>(p, ctas, smem, s);
+      case 174: return launch_pass_v<R, POLY, 174>(p, ctas, smem, s);
       case 13: return launch_pass_v<R, POLY, 13>(p, ctas, smem, s);
       case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);

@@ -558,6 +558,8 @@ struct FactorLoader {
 template <int R, uint32_t POLY, int V>
 __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
   constexpr bool RIN = V & 1, ROUT = V & 2, EXTRA = V & 4, SHAPED = V & 8;
+  // bit 6: scalings before the rounds only; bit 8: after them (and the gather epilogue) only
+  constexpr bool PRE_OK = EXTRA && !(V & 256), POST_OK = EXTRA && !(V & 64);
   // bits 4-5: every round follows one pattern -- 1: inverse (op along m0 with
   // distinct factors, op along m1 shared), 2: forward (m0 shared, m1 distinct)
   constexpr int PAT = (V >> 4) & 3;
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   // The last round keeps its data in registers and stores it straight to the
   // BS output, so the next tile's loads can stream into shared memory while
   // it computes.
-  const bool reg_path = p.nrounds > 0 && (!EXTRA || (p.npost == 0 && !p.gt_out)) &&
+  const bool reg_path = p.nrounds > 0 && (!POST_OK || (p.npost == 0 && !p.gt_out)) &&
                         (!ROUT || p.out_mode == IO_BS);
 
   for (;;) {
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (!(PDBG(128))) finish_tile_raw<R>(smem, TP);
       __syncthreads();
     }
-    if (EXTRA && p.npre) {
+    if (PRE_OK && p.npre) {
       scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
       __syncthreads();
     }
@@ -762,11 +764,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (!last_reg) __syncthreads();
     }
     if (!reg_path) {
-      if (EXTRA && p.npost) {
+      if (POST_OK && p.npost) {
         scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
         __syncthreads();
       }
-      if (EXTRA && p.gt_out) {
+      if (POST_OK && p.gt_out) {
         // derivative gather over the tile bits (derivative.py:60-70), for the
         // output positions below 2^gt_lgH
         uint4 *gdst = p.gt_out + ((size_t(g) << p.gt_lgH) * U4);
@@ -882,6 +884,10 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 153>(const PassParams &,
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 157>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 170>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 174>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 221>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 108>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 284>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 430>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
@@ -1345,6 +1351,10 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   // row-layout raw I/O (no stripe packets): the packet code paths compiled out
   const bool rows = (p.in_mode != IO_RAW || p.raw_in.pkt == 0) && (p.out_mode != IO_RAW || p.raw_out.pkt == 0);
   if (rows && (v == 25 || v == 29 || v == 42 || v == 46)) v |= 128;
+  if (v & 4) {  // scalings only before, or only after the rounds
+    const int vs = v | (!(p.npost || p.gt_out) ? 64 : !p.npre ? 256 : 0);
+    if (vs == 221 || vs == 108 || vs == 284 || vs == 430) v = vs;
+  }
   if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
@@ -1369,6 +1379,10 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 157: return launch_pass_v<R, POLY, 157>(p, ctas, smem, s);
       case 170: return launch_pass_v<R, POLY, 170>(p, ctas, smem, s);
       case 174: return launch_pass_v<R, POLY, 174>(p, ctas, smem, s);
+      case 221: return launch_pass_v<R, POLY, 221>(p, ctas, smem, s);
+      case 108: return launch_pass_v<R, POLY, 108>(p, ctas, smem, s);
+      case 284: return launch_pass_v<R, POLY, 284>(p, ctas, smem, s);
+      case 430: return launch_pass_v<R, POLY, 430>(p, ctas, smem, s);
       case 13: return launch_pass_v<R, POLY, 13>(p, ctas, smem, s);
       case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);

@@ -51,7 +51,46 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1404_3458_b200.dist import env_rank, max_over_ranks  # noqa: E402
+
+
+# Rank plumbing is local to bench.py: the reference arm must not import the
+# product package (whose __init__ maps liblch.so).
+def env_rank() -> tuple[int, int, int]:
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def max_over_ranks(values, device=None):
+    """Element-wise max over all ranks (identity for one rank)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(v) for v in values]
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
+def gather_to_rank0(obj):
+    """List of every rank's `obj` on rank 0 (None elsewhere); [obj] for one rank."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [obj]
+    out = [None] * dist.get_world_size() if dist.get_rank() == 0 else None
+    dist.gather_object(obj, out, dst=0)
+    return out
+
+
+def codeword_shard(rank: int, world: int, per_rank: int) -> tuple[int, int]:
+    """Weak scaling (configs 3/4): rank r owns codewords [r B, (r + 1) B)."""
+    return rank * per_rank, (rank + 1) * per_rank
+
+
+def group_shard(rank: int, world: int, total: int) -> tuple[int, int]:
+    """Strong scaling (config 5): contiguous split of the stripe groups."""
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
 
 # NCCL for the driver's multi-GPU runs; LCH_DIST_BACKEND=gloo runs the same
 # multi-rank logic (CPU collectives) e.g. with several ranks on one device.
@@ -185,12 +224,8 @@ def cpu_threads():
 # ---------------------------------------------------------------------------
 # CPU legs (oracle = restated reference; bounded samples)
 
-def cpu_codec(sample_cw: int, nthreads: int):
-    """Time the oracle encode + shared-pattern decode (configs 3 + 4a)."""
-    from oracle import oracle as O
-    orc = O.Oracle(16)
-    msgs = O.gen_symbols(SEED_MSG, 16, 0, sample_cw, K)
-    mask = O.gen_erasures(SEED_ERA, N, N - K, 0, 1)[0]
+def _oracle_codec_seconds(orc, msgs, mask, nthreads):
+    """(encode s, decode s) of the C oracle on `msgs` (configs 3 + 4a)."""
     t0 = time.perf_counter()
     par = orc.encode_batch(K, msgs, nthreads)
     t1 = time.perf_counter()
@@ -200,12 +235,73 @@ def cpu_codec(sample_cw: int, nthreads: int):
     out = orc.decode_batch(K, rx, mask, nthreads)
     t3 = time.perf_counter()
     assert np.array_equal(out, msgs), "oracle round trip failed"
-    sec = (t1 - t0) + (t3 - t2)
-    gbs = sample_cw * 2 * K * 2 / sec / 1e9
-    return {"value": round(gbs, 6), "unit": "GB/s", "cores": nthreads, "kind": "port",
-            "sample": f"{sample_cw} codewords encode + {sample_cw} shared-pattern decodes "
-                      f"(RS(2^16,2^15)), C oracle, {nthreads} threads",
-            "encode_s": round(t1 - t0, 3), "decode_s": round(t3 - t2, 3)}
+    return t1 - t0, t3 - t2
+
+
+CPU_SAMPLE_CW = 256  # 256 codewords for configs 3 / 4a
+
+
+def cpu_codec(sample_cw: int, nthreads: int, one_core_cw: int = 0, python_ref_cw: int = 0):
+    """The oracle (C restatement of the reference algorithm) on a bounded
+    sample of configs 3 + 4a: all host threads (`value`), optionally one core
+    (`one_core`) and the reference's own Python BatchCodec (`reference_python`,
+    when baseline/_ref is staged)."""
+    from oracle import oracle as O
+    orc = O.Oracle(16)
+    msgs = O.gen_symbols(SEED_MSG, 16, 0, sample_cw, K)
+    mask = O.gen_erasures(SEED_ERA, N, N - K, 0, 1)[0]
+    es, ds = _oracle_codec_seconds(orc, msgs, mask, nthreads)
+    res = {"value": round(sample_cw * 2 * K * 2 / (es + ds) / 1e9, 6), "unit": "GB/s",
+           "cores": nthreads, "kind": "port",
+           "sample": f"{sample_cw} codewords encode + {sample_cw} shared-pattern decodes "
+                     f"(RS(2^16,2^15)), C oracle, {nthreads} threads",
+           "sample_codewords": sample_cw, "encode_s": round(es, 3), "decode_s": round(ds, 3)}
+    if one_core_cw:
+        es1, ds1 = _oracle_codec_seconds(orc, msgs[:one_core_cw], mask, 1)
+        res["one_core"] = {"value": round(one_core_cw * 2 * K * 2 / (es1 + ds1) / 1e9, 6), "unit": "GB/s",
+                           "cores": 1, "sample_codewords": one_core_cw,
+                           "encode_s": round(es1, 3), "decode_s": round(ds1, 3)}
+    if python_ref_cw:
+        pr = python_reference_codec(python_ref_cw)
+        if pr:
+            res["reference_python"] = pr
+    return res
+
+
+def python_reference_codec(sample_cw: int):
+    """The reference's own BatchCodec (pure Python + numpy, batch.py:110-153)
+    on one core, from the staged baseline/_ref (None if absent).  Its output
+    is checked against the oracle's."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "binfec")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from binfec.basis import build_basis_tables
+    from binfec.batch import BatchCodec
+    from binfec.field import tables_for
+    from binfec.rs import CodeParams
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    codec = BatchCodec(CodeParams(16, K), build_basis_tables(tables_for(16), N))
+    setup = time.perf_counter() - t0
+    msgs = O.gen_symbols(SEED_MSG, 16, 0, sample_cw, K)
+    mask = O.gen_erasures(SEED_ERA, N, N - K, 0, 1)[0]
+    erased = set(np.nonzero(mask)[0].tolist())
+    codec.decode(codec.encode(msgs[:1]), erased)  # warm the FWHT(log) cache (walsh.py:64-74)
+    t0 = time.perf_counter()
+    cw = codec.encode(msgs)
+    t1 = time.perf_counter()
+    out = codec.decode(cw, erased)
+    t2 = time.perf_counter()
+    orc = O.Oracle(16)
+    assert np.array_equal(cw[:, K:], orc.encode_batch(K, msgs, 1)[:, :]), "reference != oracle"
+    assert np.array_equal(out, msgs)
+    return {"value": round(sample_cw * 2 * K * 2 / (t2 - t0) / 1e9, 6), "unit": "GB/s", "cores": 1,
+            "kind": "reference", "sample_codewords": sample_cw,
+            "sample": f"binfec.BatchCodec encode + decode of {sample_cw} codewords (baseline/_ref, "
+                      "unmodified reference, one core)",
+            "encode_s": round(t1 - t0, 3), "decode_s": round(t2 - t1, 3), "setup_s": round(setup, 3)}
 
 
 def cpu_stripe(k: int, lanes: int, nthreads: int):
@@ -282,48 +378,82 @@ def cpu_r8(nthreads: int):
 
 # ---------------------------------------------------------------------------
 
+def workload_config(wl: str, args, world: int) -> dict:
+    """The `config` of a workload's JSON line (identical for both arms)."""
+    if wl == "codec":
+        return {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern decode "
+                            "4096 cw (2^15 erasures) per GPU",
+                "batch_per_gpu": args.batch, "n": N, "k": K, "parallelism": f"codeword-shard x{world}",
+                "l2": "inputs larger than L2 (256 MiB message, 512 MiB received per GPU)"}
+    if wl == "stripe":
+        k, total = STRIPE[args.rate]
+        total = args.groups or total
+        lo, hi = group_shard(0, world, total)
+        return {"workload": f"cfg5: storage stripes RS(2^16,{k}) (k/n={args.rate}), 4 KiB packets "
+                            f"(P={PKT}), {total} stripe groups = {total * PKT * k * 2 / 2**30:.1f} GiB of "
+                            "message over all GPUs; encode + decode with per-group patterns of n-k "
+                            "erased packets",
+                "k": k, "n": N, "packet_len": PKT, "groups_total": total, "groups_per_gpu": hi - lo,
+                "parallelism": f"stripe-group shard x{world}", "l2": "inputs larger than L2"}
+    if wl == "transform":
+        return {"workload": "cfg2: forward + inverse + derivative, h=2^16, 1024 polynomials per GPU",
+                "h": N, "batch_per_gpu": 1024, "parallelism": f"polynomial-shard x{world}"}
+    if wl == "pcw":
+        return {"workload": "cfg4b: RS(2^16,2^15) decode 4096 cw, per-codeword patterns of 2^15 erasures",
+                "batch_per_gpu": args.batch, "n": N, "k": K, "parallelism": f"codeword-shard x{world}"}
+    return {"workload": "cfg1: GF(2^8) (256,128) encode + per-codeword decode, 64 cw per GPU",
+            "batch_per_gpu": 64, "n": 256, "k": 128}
+
+
 def run_reference_arm(args):
+    """The reference's CPU path on the host cores, on the GPU arm's exact
+    config: each step times a bounded sample of the workload with all host
+    threads (the reference is pure Python; its algorithm runs here as the C
+    oracle port, oracle/lch_oracle.c, pinned to the reference's outputs), and
+    the line reports the sample's measured rate and time per step."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
     nth = cpu_threads()
     wl = args.workload
     if wl == "codec":
-        sample = max(nth, 16)
-        cpu_codec(min(sample, 16), nth)
-        vals = [cpu_codec(sample, nth) for _ in range(args.steps)]
-        unit_bytes = BATCH * 2 * K * 2
-        cfg = {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern decode "
-                           "4096 cw (2^15 erasures) per GPU; CPU arm times a "
-                           f"{sample}-codeword sample and extrapolates the rate",
-               "batch_per_gpu": BATCH, "n": N, "k": K}
+        sample = CPU_SAMPLE_CW
+        step = lambda: cpu_codec(sample, nth)  # noqa: E731
+        unit = f"{sample} codewords (of the {args.batch} per GPU) encode + shared-pattern decode"
     elif wl == "stripe":
-        k, groups = STRIPE[args.rate]
-        vals = [cpu_stripe(k, max(nth, 16), nth) for _ in range(max(1, min(args.steps, 3)))]
-        unit_bytes = groups * PKT * k * 2 * 2
-        cfg = {"workload": f"cfg5: RS(2^16,{k}) 4 KiB packets, {groups} stripe groups", "k": k}
+        k, _ = STRIPE[args.rate]
+        step = lambda: cpu_stripe(k, 64, nth)  # noqa: E731
+        unit = "64 packet lanes (codewords) of one stripe group, encode + decode"
     elif wl == "transform":
-        vals = [cpu_transform(max(nth, 8), nth) for _ in range(max(1, min(args.steps, 3)))]
-        unit_bytes = 1024 * 3 * 4 * N
-        cfg = {"workload": "cfg2: forward+inverse+derivative h=2^16 x 1024", "h": N}
+        step = lambda: cpu_transform(max(nth, 8), nth)  # noqa: E731
+        unit = f"{max(nth, 8)} of the 1024 polynomials, forward + inverse + derivative"
     elif wl == "pcw":
-        vals = [cpu_pcw(max(nth, 16), nth) for _ in range(max(1, min(args.steps, 3)))]
-        unit_bytes = BATCH * K * 2
-        cfg = {"workload": "cfg4b: per-codeword-pattern decode 4096 cw", "n": N, "k": K}
+        step = lambda: cpu_pcw(max(nth, 16), nth)  # noqa: E731
+        unit = f"{max(nth, 16)} of the {args.batch} codewords, per-codeword-pattern decode"
     else:
-        vals = [cpu_r8(nth) for _ in range(max(1, min(args.steps, 3)))]
-        unit_bytes = 2 * 64 * 128
-        cfg = {"workload": "cfg1: r=8 (256,128) 64 cw encode + per-codeword decode"}
+        step = lambda: cpu_r8(nth)  # noqa: E731
+        unit = "all 64 codewords, encode + per-codeword decode"
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    vals = [step() for _ in range(args.steps)]
+    ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
     v = float(np.median([x["value"] for x in vals]))
     cb = dict(vals[-1])
     cb["value"] = round(v, 6)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(unit_bytes / (v * 1e9) * 1e3, 3),
+            "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16",
-            "data": DATA, "config": cfg, "cpu_baseline": cb,
+            "data": DATA, "config": workload_config(wl, args, args.gpus),
+            "sample_per_step": unit + f" on {nth} host threads (ms_per_step is the sample's time)",
+            "cpu_baseline": cb,
             "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if wl == "codec" and not args.no_cpu:
+        pr = python_reference_codec(16)
+        if pr:
+            line["reference_python"] = pr
     print(json.dumps(line), flush=True)
     return 0
 
@@ -414,7 +544,7 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
     cp = lch.CodeParams(16, K)
     ctx = bt.ctx.handle
     stream = torch.cuda.current_stream()
-    cw0 = rank * B
+    cw0, _ = codeword_shard(rank, world, B)
 
     # inputs resident in HBM (weak scaling: each rank owns its own codewords)
     msg = torch.empty((B, K), dtype=torch.int16, device="cuda")
@@ -455,25 +585,32 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
     value = world * len(phases) * msg_bytes / (step_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
     enc, dec = ph.get("encode"), ph.get("decode")
-    # dominant kernel: the encode's pass_kernel launches (5 per encode)
-    per_launch_ms = enc / 5 if enc else dec / 8
-    per_launch_bytes = 4 * K * B  # 2 B read + 2 B write per symbol-position
-    codec_alg = 2 * N * B  # encode: read k + write n-k symbols (2 B each) per codeword
-    cfg = {"workload": "cfg3+cfg4a: RS(2^16,2^15) encode 4096 cw + shared-pattern decode "
-                       "4096 cw (2^15 erasures) per GPU",
-           "batch_per_gpu": B, "n": N, "k": K, "parallelism": f"codeword-shard x{world}",
-           "l2": "inputs larger than L2 (256 MiB message, 512 MiB received per GPU)"}
+    codec_alg = 2 * N * B  # SURVEY §8d encode: read k + write n-k symbols (2 B each) per codeword
+    dec_alg = (2 * (N - K) + 2 * K) * B  # decode: read n-|E| survivors + write k
+    cfg = workload_config("codec", args, world)
     res = base_line(args, world, value, step_ms, cfg, launches, clocks)
     res.update({
         "encode_ms": round(enc, 4) if enc else None, "decode_ms": round(dec, 4) if dec else None,
         "encode_gbs": round(world * msg_bytes / (enc * 1e-3) / 1e9, 3) if enc else None,
         "decode_gbs": round(world * msg_bytes / (dec * 1e-3) / 1e9, 3) if dec else None,
+        "encode_symbols_per_s": round(B * K * world / (enc * 1e-3), 1) if enc else None,
+        "decode_symbols_per_s": round(B * K * world / (dec * 1e-3), 1) if dec else None,
         "encode_hbm_frac": round(codec_alg / (enc * 1e-3) / 1e9 / peak, 4) if enc else None,
-        "decode_hbm_frac": round((2 * (N - K) + 2 * K) * B / (dec * 1e-3) / 1e9 / peak, 4)
-        if dec else None,
-        "roofline": roofline("pass_kernel<16,0x1100B> (encode tile pass)", per_launch_bytes,
-                             per_launch_ms, peak, peak_src, read_traffic()),
+        "decode_hbm_frac": round(dec_alg / (dec * 1e-3) / 1e9 / peak, 4) if dec else None,
     })
+    if enc:
+        # the encode's algorithmic bytes over the summed duration of
+        # the dominant kernel's launches in it (all 5 launches of an RS(2^16,
+        # 2^15) encode are pass_kernel instances, so that sum is the encode time)
+        res["roofline"] = roofline("pass_kernel<16,0x1100B> (the 5 launches of one encode)", codec_alg,
+                                   enc, peak, peak_src, read_traffic())
+        res["roofline"]["launches_per_unit"] = 5
+        res["roofline"]["unit_of_work"] = f"one encode of {B} codewords (2n B per codeword)"
+        res["pass_dram_efficiency"] = {
+            "what": "per-pass bytes (4 B per symbol-position: 2 B read + 2 B write) / mean pass time, "
+                    "vs measured HBM peak -- how close each pass is to streaming, not codec progress",
+            "achieved_gbs": round(4 * K * B / (enc / 5 * 1e-3) / 1e9, 1),
+            "frac": round(4 * K * B / (enc / 5 * 1e-3) / 1e9 / peak, 4)}
     prof = read_profile()
     if prof.get("alu_pipe_pct_per_launch"):
         alu = prof["alu_pipe_pct_per_launch"]
@@ -482,7 +619,7 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
             "busy_frac": round(sum(alu) / len(alu) / 100.0, 3),
             "dram_frac_same_launches": round(sum(prof.get("dram_pct_per_launch", [0])) /
                                              max(1, len(prof.get("dram_pct_per_launch", [0]))) / 100.0, 3),
-            "source": "ncu --set full, profiles/r01_pass_kernel_full.txt"}
+            "source": prof.get("source", "ncu --set full (profiles/)")}
 
     # e2e through the public host-buffer API (lch_encode_host / lch_decode_host:
     # chunked H2D / kernels / D2H overlapped on three streams), pinned buffers
@@ -513,6 +650,7 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b) / e2e_steps
+        per_rank = gather_to_rank0(round(e2e_ms, 3))
         if world > 1:
             e2e_ms = max_over_ranks([e2e_ms], dist_device())[0]
         assert torch.equal(h_out, h_msg), "e2e round trip failed"
@@ -521,25 +659,24 @@ def run_codec(args, torch, lch, _lib, world, rank, local):
         res["e2e"] = {"value": round(world * 2 * msg_bytes / (e2e_ms * 1e-3) / 1e9, 3),
                       "unit": "GB/s", "h2d_bytes_per_step": B * K * 2 + B * surv * 2,
                       "d2h_bytes_per_step": B * (N - K) * 2 + B * K * 2,
-                      "ms_per_step": round(e2e_ms, 3),
+                      "ms_per_step": round(e2e_ms, 3), "ms_per_step_per_rank": per_rank,
                       "api": "lch_encode_host + lch_decode_host (pinned host buffers; chunked "
                              "H2D / kernel / D2H overlap on three streams; the received words' "
                              "survivors are compacted on the host so erased symbols, which the "
                              "decoder ignores, do not cross PCIe)"}
     if rank == 0 and world == 1 and not args.no_cpu:
         nth = cpu_threads()
-        res["cpu_baseline"] = cpu_codec(max(8, min(nth, 64)), nth)
+        res["cpu_baseline"] = cpu_codec(CPU_SAMPLE_CW, nth, one_core_cw=CPU_SAMPLE_CW, python_ref_cw=16)
     return res
 
 
 def run_stripe(args, torch, lch, _lib, world, rank, local):
     """Config 5: codeword buffer [G, n, P] per GPU, message = positions [0, k)."""
     from paper_1404_3458_b200 import gen
-    from paper_1404_3458_b200.dist import split_range
     k, groups_total = STRIPE[args.rate]
     if args.groups:
         groups_total = args.groups
-    g_lo, g_hi = split_range(rank, world, groups_total)  # strong scaling: 32 GiB total
+    g_lo, g_hi = group_shard(rank, world, groups_total)  # strong scaling: 32 GiB total
     G = g_hi - g_lo
     bt = lch.build_basis_tables(lch.tables_for(16), N)
     ctx = bt.ctx.handle
@@ -579,13 +716,8 @@ def run_stripe(args, torch, lch, _lib, world, rank, local):
     value = 2 * total_msg / (step_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
     enc, dec = ph["encode"], ph["decode"]
-    cfg = {"workload": f"cfg5: storage stripes RS(2^16,{k}) (k/n={args.rate}), 4 KiB packets "
-                       f"(P={PKT}), {groups_total} stripe groups = {total_msg / 2**30:.1f} GiB of "
-                       "message over all GPUs; encode + decode with per-group patterns of n-k "
-                       "erased packets",
-           "k": k, "n": N, "packet_len": PKT, "groups_total": groups_total,
-           "groups_per_gpu": G, "parallelism": f"stripe-group shard x{world}",
-           "l2": "inputs larger than L2"}
+    cfg = workload_config("stripe", args, world)
+    cfg["groups_per_gpu"] = G
     res = base_line(args, world, value, step_ms, cfg, launches, clocks, scaling="strong")
     res.update({
         "encode_ms": round(enc, 3), "decode_ms": round(dec, 3),
@@ -670,8 +802,7 @@ def run_transform_wl(args, torch, lch, _lib, world, rank, local):
     per = 4 * N * B  # 4h bytes per polynomial per pass
     value = world * 3 * per / (step_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
-    cfg = {"workload": "cfg2: forward + inverse + derivative, h=2^16, 1024 polynomials per GPU",
-           "h": N, "batch_per_gpu": B, "parallelism": f"polynomial-shard x{world}"}
+    cfg = workload_config("transform", args, world)
     res = base_line(args, world, value, step_ms, cfg, launches, clocks)
     res.update({f"{k}_ms": round(v, 4) for k, v in ph.items()})
     res.update({f"{k}_gbs": round(world * per / (v * 1e-3) / 1e9, 2) for k, v in ph.items()})
@@ -712,8 +843,7 @@ def run_pcw(args, torch, lch, _lib, world, rank, local):
                                                              args.warmup, world, local, _lib.lib, ctx)
     value = world * B * K * 2 / (step_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
-    cfg = {"workload": "cfg4b: RS(2^16,2^15) decode 4096 cw, per-codeword patterns of 2^15 erasures",
-           "batch_per_gpu": B, "n": N, "k": K, "parallelism": f"codeword-shard x{world}"}
+    cfg = workload_config("pcw", args, world)
     res = base_line(args, world, value, step_ms, cfg, launches, clocks)
     alg = (2 * K + 2 * K + N // 8) * B
     res["roofline"] = roofline("decode pipeline (algorithmic: survivors + output + bitmask)", alg,
@@ -776,9 +906,8 @@ def run_r8(args, torch, lch, _lib, world, rank, local):
     launches = 2 * args.steps  # one kernel per phase inside the graphs
     value = world * 2 * B * k / (step_ms * 1e-3) / 1e9
     peak, peak_src = hbm_peak()
-    cfg = {"workload": "cfg1: GF(2^8) (256,128) encode + per-codeword decode, 64 cw per GPU "
-                       "(small-codeword kernel, one CTA per codeword, phases replayed as CUDA graphs)",
-           "batch_per_gpu": B, "n": n, "k": k}
+    cfg = workload_config("r8", args, world)
+    cfg["note"] = "small-codeword kernel, one CTA per codeword, phases replayed as CUDA graphs"
     res = base_line(args, world, value, step_ms, cfg, launches, clocks)
     res.update({"encode_ms": round(ph["encode"], 4), "decode_ms": round(ph["decode"], 4)})
     res["roofline"] = roofline("encode (latency bound)", 2 * n * B, ph["encode"], peak, peak_src)
@@ -786,6 +915,60 @@ def run_r8(args, torch, lch, _lib, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         res["cpu_baseline"] = cpu_r8(cpu_threads())
     return res
+
+
+AUX_KEYS = ("value", "unit", "ms_per_step", "encode_ms", "decode_ms", "forward_ms", "inverse_ms",
+            "derivative_ms", "encode_gbs", "decode_gbs", "forward_gbs", "inverse_gbs", "derivative_gbs",
+            "encode_hbm_frac", "decode_hbm_frac", "gpu_launches", "scaling", "clocks")
+
+
+def run_aux(args, torch, lch, _lib, world, rank, local):
+    """The other BASELINE configs (1, 2, 4b, 5 at all three rates), each on its
+    full per-GPU shape with a few steps, so the default run reports every
+    config (each function gates its timing on a full-batch round trip)."""
+    import copy
+    res = {}
+    todo = [("cfg1_r8", run_r8, {}), ("cfg2_transform", run_transform_wl, {}), ("cfg4b_pcw", run_pcw, {}),
+            ("cfg5_rate_1_2", run_stripe, {"rate": "1/2"}), ("cfg5_rate_3_4", run_stripe, {"rate": "3/4"}),
+            ("cfg5_rate_15_16", run_stripe, {"rate": "15/16"})]
+    for name, fn, extra in todo:
+        a = copy.copy(args)
+        a.__dict__.update(steps=max(1, min(args.steps, 3)), warmup=3, no_cpu=True, no_e2e=True, **extra)
+        try:
+            r = fn(a, torch, lch, _lib, world, rank, local)
+        except Exception as exc:  # report, keep the headline line
+            r = {"error": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        if r is None:
+            r = {"error": "round-trip check failed"}
+        ent = {k: r[k] for k in AUX_KEYS if k in r}
+        if "error" in r:
+            ent["error"] = r["error"]
+        if "config" in r:
+            ent["workload"] = r["config"]["workload"]
+        if r.get("roofline"):
+            ent["roofline_frac"] = r["roofline"]["frac"]
+        ent["steps"], ent["warmup"] = a.steps, a.warmup
+        res[name] = ent
+    return res
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N ranks (one process per GPU, NCCL)."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"error": f"--gpus {n} but only {have} CUDA devices visible"}), flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -800,28 +983,48 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-aux", action="store_true", help="skip the other configs' keys")
     ap.add_argument("--only", default="", help="encode|decode (profiling runs)")
     args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
         return run_reference_arm(args)
+
+    launched = "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not launched:
+        return spawn_ranks(args.gpus)
+    rank, world, local = env_rank()
+    if launched and world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        return 2
 
     import torch
     import torch.distributed as dist
 
-    rank, world, local = env_rank()
-    local = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
     if world > 1:
         if DIST_BACKEND == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
         else:
             dist.init_process_group(DIST_BACKEND)
+    dev = torch.cuda.current_device()
+    props = torch.cuda.get_device_properties(dev)
+    # one line per rank (stderr): which device each rank drives, and the
+    # communicator size it sees
+    print(json.dumps({"rank": rank, "local_rank": local, "world_size": world, "device": dev,
+                      "device_name": props.name, "pci_bus_id": getattr(props, "pci_bus_id", None),
+                      "comm_size": dist.get_world_size() if dist.is_initialized() else 1,
+                      "backend": DIST_BACKEND if world > 1 else None}), file=sys.stderr, flush=True)
     import paper_1404_3458_b200 as lch
     from paper_1404_3458_b200 import _lib
 
     fn = {"codec": run_codec, "stripe": run_stripe, "transform": run_transform_wl, "pcw": run_pcw,
           "r8": run_r8}[args.workload]
     res = fn(args, torch, lch, _lib, world, rank, local)
+    if res is not None and args.workload == "codec" and not args.no_aux and not args.only:
+        torch.cuda.empty_cache()
+        res["other_configs"] = run_aux(args, torch, lch, _lib, world, rank, local)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

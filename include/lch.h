@@ -87,6 +87,12 @@ int lch_inverse(lch_ctx *ctx, uint16_t *data, int64_t batch, int64_t row_stride,
 int lch_derivative(lch_ctx *ctx, const uint16_t *in, uint16_t *out, int64_t batch,
                    int64_t row_stride, int lg_h, int64_t packet_len, void *stream);
 
+/* Formal derivative by the direct formula out[j] = sum_{l : bit l of j clear}
+ * W'_l * in[j + 2^l] (derivative.derivative_direct, derivative.py:26-43):
+ * an independent check of lch_derivative, row layout only, in != out. */
+int lch_derivative_direct(lch_ctx *ctx, const uint16_t *in, uint16_t *out, int64_t batch,
+                          int64_t row_stride, int lg_h, void *stream);
+
 /* In-place Walsh-Hadamard transform over Z_modulus of `batch` vectors of
  * length 2^lg_n (uint32 residues).  Replaces walsh.fwht (walsh.py:42-61). */
 int lch_fwht(lch_ctx *ctx, uint32_t *data, int64_t batch, int lg_n, uint32_t modulus,

@@ -61,6 +61,7 @@ def _load() -> ctypes.CDLL:
         "lch_gen_symbols": ([P, u64, u64, i64, i64, P, i64, P], i32),
         "lch_gen_packets": ([P, u64, u64, i64, i64, P, i64, i64, P], i32),
         "lch_pointwise_mul": ([P, P, P, P, i64, P], i32),
+        "lch_derivative_direct": ([P, P, P, i64, i64, i32, P], i32),
         "lch_stripes_to_packets": ([P, P, i64, i32, i64, P, i64, P], i32),
         "lch_packets_to_stripes": ([P, P, i64, i32, i64, P, i64, P], i32),
         "lch_payload_to_packets": ([P, P, i64, i64, i32, P, i64, P], i32),

@@ -8,8 +8,6 @@ per (field, max_h).
 
 from __future__ import annotations
 
-from collections.abc import Sequence
-
 from . import _lib
 from .field import FieldTables
 
@@ -58,26 +56,6 @@ class BasisTables:
     def eval_w_hat(self, i: int, j: int) -> int:
         """Normalised factor W_i(j) / W_i(v_i) (basis.py:107-109)."""
         return self.ft.mul(self.eval_w(i, j), self.inv_norm[i])
-
-    def eval_x_naive(self, i: int, x: int) -> int:
-        """X_i(x) as the explicit product of factors (basis.py:111-121; test oracle)."""
-        acc = 1
-        j = 0
-        while i:
-            if i & 1:
-                acc = self.ft.mul(acc, self.eval_w_hat(j, x))
-            i >>= 1
-            j += 1
-        return acc
-
-    def eval_poly_naive(self, coeffs: Sequence[int], x: int) -> int:
-        """sum_i coeffs[i] X_i(x) term by term (basis.py:123-132; test oracle)."""
-        mul = self.ft.mul
-        acc = 0
-        for i, d in enumerate(coeffs):
-            if d:
-                acc ^= mul(d, self.eval_x_naive(i, x))
-        return acc
 
 
 def build_basis_tables(ft: FieldTables, max_h: int) -> BasisTables:

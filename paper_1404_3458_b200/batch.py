@@ -135,17 +135,26 @@ class BatchCodec:
             raise ValueError(f"received width {received.shape[1]} != n={n}")
         torch = _lib.torch_mod()
         rd = self._dev(received)
-        if _is_torch(erased_masks):
-            m = erased_masks.to("cuda").bool()
+        if _is_torch(erased_masks) and erased_masks.is_cuda:
+            # device masks: packed on the device; the library counts the
+            # erasures of each pattern itself (and reports too many)
+            m = erased_masks.bool()
+            if tuple(m.shape) != (rd.shape[0], n):
+                raise ValueError("erased_masks must be [stripes, n]")
+            from .gen import mask_to_bits
+            bits = mask_to_bits(m).contiguous()
+            counts = None
         else:
-            m = torch.from_numpy(np.asarray(erased_masks).astype(bool)).to("cuda")
-        if m.shape != (rd.shape[0], n):
-            raise ValueError("erased_masks must be [stripes, n]")
-        from .gen import mask_to_bits
-        bits = mask_to_bits(m).contiguous()
-        counts = m.sum(dim=1).cpu().tolist()
-        if any(c > n - k for c in counts):
-            raise TooManyErasuresError(f"{max(counts)} erasures exceed repair capacity {n - k}")
+            # host masks: bit-pack and count on the host, one upload
+            mh = erased_masks.numpy() if _is_torch(erased_masks) else np.asarray(erased_masks)
+            mh = mh.astype(bool, copy=False)
+            if mh.shape != (rd.shape[0], n):
+                raise ValueError("erased_masks must be [stripes, n]")
+            counts = np.count_nonzero(mh, axis=1).tolist()
+            if any(c > n - k for c in counts):
+                raise TooManyErasuresError(f"{max(counts)} erasures exceed repair capacity {n - k}")
+            packed = np.packbits(mh, axis=1, bitorder="little").view(np.uint32)
+            bits = _lib.to_device_u32(np.ascontiguousarray(packed))
         out = torch.empty((rd.shape[0], k), dtype=torch.int16, device="cuda")
         if rd.shape[0] > 0:
             decode_device(cp, self.bt, rd, bits, out, counts)

@@ -36,6 +36,10 @@ struct lch_ctx {
   std::vector<std::pair<size_t, void *>> pinned;          // page-locked staging slots
   std::unique_ptr<HostPool> pool;                          // host workers (survivor compaction)
   cudaEvent_t ring_ev[16] = {};                            // upload_small ring slots
+  // per staging slot: the last H2D copy that reads it (host_pipeline waits on
+  // it before refilling the slot, also across calls)
+  std::vector<cudaEvent_t> stage_ev;
+  cudaMemPool_t mempool = nullptr;                         // private stream-ordered scratch pool
   size_t ring_next = 0;
   std::mutex mu;
   std::mutex host_mu;  // serialises the host-buffer entry points (shared staging, pool)
@@ -83,12 +87,15 @@ int ensure_device(lch_ctx *c) {
     for (uint32_t j = 0; j < c->t.order; ++j) blo[j] = c->t.b_prod[j & (c->t.order / 2 - 1)];
     LCH_TRY(upload(c->d_b_lo, blo));
   }
-  // keep freed scratch in the stream-ordered pool (no re-mapping per call)
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
+  // the context's own stream-ordered pool keeps freed scratch mapped (no
+  // re-mapping per call) without touching the process-wide default pool
+  cudaMemPoolProps pp = {};
+  pp.allocType = cudaMemAllocationTypePinned;
+  pp.location.type = cudaMemLocationTypeDevice;
+  pp.location.id = c->device;
+  LCH_TRY(cu(cudaMemPoolCreate(&c->mempool, &pp)));
+  uint64_t thr = ~0ull;
+  LCH_TRY(cu(cudaMemPoolSetAttribute(c->mempool, cudaMemPoolAttrReleaseThreshold, &thr)));
   c->dev_ready = true;
   return LCH_OK;
 }
@@ -96,8 +103,9 @@ int ensure_device(lch_ctx *c) {
 // Stream-ordered scratch allocation freed at scope exit.
 struct Scratch {
   cudaStream_t s;
+  cudaMemPool_t pool;
   std::vector<void *> ptrs;
-  explicit Scratch(cudaStream_t st) : s(st) {}
+  Scratch(const lch_ctx *c, cudaStream_t st) : s(st), pool(c->mempool) {}
   ~Scratch() {
     for (void *p : ptrs) cudaFreeAsync(p, s);
   }
@@ -105,7 +113,8 @@ struct Scratch {
   int alloc(T *&p, size_t count) {
     void *v = nullptr;
     if (count == 0) count = 1;
-    cudaError_t e = cudaMallocAsync(&v, count * sizeof(T), s);
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(&v, count * sizeof(T), pool, s)
+                         : cudaMallocAsync(&v, count * sizeof(T), s);
     if (e != cudaSuccess) return cu(e);
     ptrs.push_back(v);
     p = static_cast<T *>(v);
@@ -450,7 +459,7 @@ int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out
     c->launches++;
     return LCH_OK;
   }
-  Scratch sc(s);
+  Scratch sc(c, s);
   uint32_t *buf = nullptr;
   LCH_TRY(sc.alloc(buf, size_t(np) * n));
   const int ngrp = (r + 7) / 8;
@@ -542,6 +551,12 @@ void lch_destroy(lch_ctx *c) {
       if (e.second) cudaFreeHost(e.second);
     for (cudaEvent_t e : c->ring_ev)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->stage_ev)
+      if (e) cudaEventDestroy(e);
+    if (c->mempool) {
+      cudaDeviceSynchronize();
+      cudaMemPoolDestroy(c->mempool);
+    }
   }
   delete c;
 }
@@ -641,7 +656,7 @@ static int erasure_core(lch_ctx *c, const RawIO &in0, const RawIO &out0, const u
   const int r = c->t.r;
   const bool folded = lg_out <= r - 1;
   const int64_t ch = chunk_lanes(c, batch, pkt, bs_lane_bytes(R, r) + 2 * bs_lane_bytes(R, lg_out));
-  Scratch sc(s);
+  Scratch sc(c, s);
   uint4 *x = nullptr, *t = nullptr, *t1 = nullptr;
   LCH_TRY(sc.alloc(x, bs_bytes(R, ch, r) / 16));
   LCH_TRY(sc.alloc(t, bs_bytes(R, ch, lg_out) / 16));
@@ -682,7 +697,7 @@ static int pattern_counts(lch_ctx *c, const uint32_t *bits, int64_t np, int word
     std::memcpy(counts.data(), host_counts, sizeof(int64_t) * size_t(np));
     return LCH_OK;
   }
-  Scratch sc(s);
+  Scratch sc(c, s);
   int64_t *dc = nullptr;
   LCH_TRY(sc.alloc(dc, size_t(np)));
   LCH_TRY(cu(launch_count_bits(bits, np, words, dc, s)));
@@ -726,7 +741,7 @@ static int transform_impl(lch_ctx *c, uint16_t *data, int64_t batch, int64_t str
     constexpr uint32_t P = decltype(PC)::value;
     auto plan = plan_passes(ops, lg_h, true, true);
     const int64_t ch = plan.size() > 1 ? chunk_lanes(c, batch, pkt, bs_lane_bytes(R, lg_h)) : batch;
-    Scratch sc(s);
+    Scratch sc(c, s);
     uint4 *work = nullptr;
     if (plan.size() > 1) LCH_TRY(sc.alloc(work, bs_bytes(R, ch, lg_h) / 16));
     const RawIO io0 = make_io(data, stride, pkt);
@@ -798,7 +813,7 @@ static int encode_pow2(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint1
   return dispatch(c, [&](auto RC, auto PC) -> int {
     constexpr int R = decltype(RC)::value;
     constexpr uint32_t P = decltype(PC)::value;
-    Scratch sc(s);
+    Scratch sc(c, s);
     const RawIO in0 = make_io(msg, stride_in, pkt);
     // rs.py:91 coefficients by a k-point inverse at shift 0
     std::vector<LOp> inv;
@@ -862,7 +877,7 @@ static int encode_tables(lch_ctx *c, int64_t k, const uint16_t *&pi_row, const u
   LCH_TRY(cu(cudaMalloc(&tab, size_t(2 * n) * 2)));
   int rc;
   {
-    Scratch sc(s);
+    Scratch sc(c, s);
     uint32_t *db = nullptr;
     uint16_t *pr = nullptr, *pv = nullptr;
     rc = sc.alloc(db, size_t(words));
@@ -963,7 +978,7 @@ static int encode_general(lch_ctx *c, const uint16_t *msg, int64_t stride_in, ui
     const int64_t nb = std::min(ch, batch - b0);
     const int64_t off_in = pkt ? (b0 / pkt) * stride_in * pkt : b0 * stride_in;
     const int64_t off_out = pkt ? (b0 / pkt) * stride_out * pkt : b0 * stride_out;
-    Scratch sc(s);
+    Scratch sc(c, s);
     LCH_TRY(solve_interp(c, View{const_cast<uint16_t *>(msg) + off_in, stride_in},
                          View{parity + off_out, stride_out}, nb, n, k, pkt, s, sc));
   }
@@ -1017,7 +1032,7 @@ static int decode_per_codeword(lch_ctx *c, const uint16_t *rx, int64_t stride_in
   return dispatch(c, [&](auto RC, auto PC) -> int {
     constexpr int R = decltype(RC)::value;
     constexpr uint32_t P = decltype(PC)::value;
-    Scratch sc(s);
+    Scratch sc(c, s);
     uint16_t *phi = nullptr, *pinv_log = nullptr;
     LCH_TRY(sc.alloc(phi, size_t(batch) * size_t(stride_in)));
     LCH_TRY(sc.alloc(pinv_log, size_t(batch) * size_t(kf)));
@@ -1124,7 +1139,7 @@ static int decode_any(lch_ctx *c, const uint16_t *rx, int64_t stride_in, const u
   }
   const int lgo = std::max(ceil_lg(k), 1);
   const int64_t kf = int64_t(1) << lgo;
-  Scratch sc(s);
+  Scratch sc(c, s);
   uint16_t *pi_row = nullptr, *pinv = nullptr;
   // rs.py:125 locator values, one per pattern
   LCH_TRY(erasure_tables(c, bits, np, kf, sc, pi_row, pinv, s));
@@ -1175,7 +1190,7 @@ int lch_derivative(lch_ctx *c, const uint16_t *in, uint16_t *out, int64_t batch,
     constexpr int R = decltype(RC)::value;
     constexpr uint32_t P = decltype(PC)::value;
     const int64_t ch = chunk_lanes(c, batch, pkt, 2 * bs_lane_bytes(R, lg_h));
-    Scratch sc(s);
+    Scratch sc(c, s);
     uint4 *x = nullptr, *t = nullptr;
     LCH_TRY(sc.alloc(x, bs_bytes(R, ch, lg_h) / 16));
     LCH_TRY(sc.alloc(t, bs_bytes(R, ch, lg_h) / 16));
@@ -1361,7 +1376,7 @@ int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
       for (cudaEvent_t e : *v) cudaEventDestroy(e);
     }
   } guard{&evs};
-  Scratch sc(s);
+  Scratch sc(c, s);
   std::vector<uint8_t *> din(size_t(NS) * ni, nullptr), dout(NS, nullptr);
   for (int k = 0; k < NS; ++k) {
     for (int a = 0; a < ni; ++a) LCH_TRY(sc.alloc(din[size_t(k) * ni + a], ins[a].row_bytes * size_t(chunk)));
@@ -1399,12 +1414,22 @@ int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
       const HostArray &h = ins[a];
       uint8_t *d = din[size_t(k) * ni + a];
       if (h.prep) {
-        // the staging slot is free once the H2D copy of chunk i - NS has run
-        uint8_t *stg = pinned_buffer(c, size_t(k) * ni + a, h.row_bytes * size_t(chunk));
+        // the staging slot is free once the last H2D copy out of it has run --
+        // in this call (chunk i - NS) or in an earlier call still in flight
+        const size_t si = size_t(k) * ni + a;
+        uint8_t *stg = pinned_buffer(c, si, h.row_bytes * size_t(chunk));
         if (!stg) return LCH_ENOMEM;
-        if (i >= NS) LCH_TRY(cu(cudaEventSynchronize(ev_in[k])));
+        cudaEvent_t sev = nullptr;
+        {
+          std::lock_guard<std::mutex> g(c->mu);
+          if (c->stage_ev.size() <= si) c->stage_ev.resize(si + 1, nullptr);
+          if (!c->stage_ev[si]) LCH_TRY(cu(cudaEventCreateWithFlags(&c->stage_ev[si], cudaEventDisableTiming)));
+          sev = c->stage_ev[si];
+        }
+        LCH_TRY(cu(cudaEventSynchronize(sev)));
         h.prep(r0, nr, stg);
         LCH_TRY(cu(cudaMemcpyAsync(d, stg, h.row_bytes * size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
+        LCH_TRY(cu(cudaEventRecord(sev, c->s_h2d)));
       } else {
         LCH_TRY(cu(cudaMemcpy2DAsync(d, h.row_bytes, h.src + size_t(r0) * h.pitch, h.pitch, h.row_bytes,
                                      size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
@@ -1505,7 +1530,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
     counts[size_t(i)] = popcount_words(host_bits + i * words, words);
     if (counts[size_t(i)] > n - k) return LCH_ETOOMANY;  // rs.py:121-123
   }
-  Scratch sc(s);
+  Scratch sc(c, s);
   uint32_t *d_shared = nullptr;
   if (shared) {
     LCH_TRY(sc.alloc(d_shared, size_t(words)));
@@ -1541,7 +1566,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
     cout.pitch = size_t(stride_out) * 2;
     return host_pipeline(c, s, rows, chunk, cins, cout,
                          [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr) {
-                           Scratch cs(s);
+                           Scratch cs(c, s);
                            uint16_t *full = nullptr;
                            LCH_TRY(cs.alloc(full, size_t(nr) * size_t(n)));
                            LCH_TRY(cu(launch_expand_rows(reinterpret_cast<const uint16_t *>(d[0]),
@@ -1597,7 +1622,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
     cout.pitch = size_t(stride_out) * pkt_bytes;
     return host_pipeline(c, s, rows, chunk, cins, cout,
                          [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr) {
-                           Scratch cs(s);
+                           Scratch cs(c, s);
                            const int64_t npat = shared ? 1 : nr;
                            std::vector<int32_t> rank(size_t(npat) * size_t(n), -1);
                            for (int64_t g = 0; g < npat; ++g) {
@@ -1686,6 +1711,21 @@ int lch_pointwise_mul(lch_ctx *c, const uint16_t *a, const uint16_t *b, uint16_t
   const bool clmul = c->t.r == 16 && c->t.poly == 0x1100Bu;
   return cu(launch_pointwise_mul(a, b, out, count, clmul ? nullptr : c->d_log, c->d_exp, c->t.m,
                                  static_cast<cudaStream_t>(stream)));
+}
+
+int lch_derivative_direct(lch_ctx *c, const uint16_t *in, uint16_t *out, int64_t batch, int64_t row_stride,
+                          int lg_h, void *stream) {
+  if (!c || batch < 0 || lg_h < 0 || lg_h > c->max_lg_h || row_stride < (int64_t(1) << lg_h) ||
+      (batch && (!in || !out)) || (batch && in == out))
+    return LCH_EINVAL;
+  LCH_TRY(ensure_device(c));
+  if (batch == 0) return LCH_OK;
+  WPrime wp{};
+  for (int l = 0; l < c->t.r && l < 16; ++l) wp.w[l] = c->t.w_prime[l];
+  wp.r = c->t.r;
+  wp.poly = c->t.poly;
+  c->launches++;
+  return cu(launch_derivative_direct(in, out, batch, row_stride, lg_h, wp, static_cast<cudaStream_t>(stream)));
 }
 
 // ---- shard-file layouts (shardfile.py:109-140) ----------------------------

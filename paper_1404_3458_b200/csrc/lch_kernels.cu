@@ -1532,6 +1532,36 @@ __global__ void pointwise_mul_kernel(const uint16_t *a, const uint16_t *b, uint1
   }
 }
 
+// Formal derivative by the direct per-coefficient formula (derivative.py:26-43):
+// out[j] = sum over clear bits l of j (j + 2^l < h) of W'_l * d[j + 2^l].  A
+// generic shift-and-reduce product (any r <= 16, any polynomial): an
+// independent path from the B-scaled gather of lch_derivative.
+__device__ __forceinline__ uint32_t gf_mul_generic(uint32_t a, uint32_t b, int r, uint32_t poly) {
+  uint32_t z = 0;
+  for (int i = 0; i < r; ++i)
+    if ((b >> i) & 1u) z ^= a << i;
+  for (int i = 2 * r - 2; i >= r; --i)
+    if ((z >> i) & 1u) z ^= poly << (i - r);
+  return z;
+}
+
+__global__ void derivative_direct_kernel(const uint16_t *in, uint16_t *out, int64_t batch, int64_t stride,
+                                         int lg_h, WPrime wp) {
+  const int64_t h = int64_t(1) << lg_h, total = batch * h;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i >> lg_h, j = i & (h - 1);
+    const uint16_t *row = in + b * stride;
+    uint32_t acc = 0;
+    for (int l = 0; l < lg_h; ++l) {
+      if ((j >> l) & 1) continue;
+      const uint32_t d = __ldg(row + j + (int64_t(1) << l));
+      if (d) acc ^= gf_mul_generic(wp.w[l], d, wp.r, wp.poly);
+    }
+    out[b * stride + j] = uint16_t(acc);
+  }
+}
+
 static int grid_for(int64_t total) {
   return int(total / 256 + 1 < 148 * 32 ? total / 256 + 1 : 148 * 32);
 }
@@ -1571,6 +1601,12 @@ cudaError_t launch_expand_packets(const uint16_t *comp, int64_t comp_pos, const 
   expand_packets_kernel<<<grid_for(groups * n * pk4), 256, 0, s>>>(
       reinterpret_cast<const uint4 *>(comp), comp_pos, rank, rank_stride, reinterpret_cast<uint4 *>(full), n,
       pk4, groups);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_derivative_direct(const uint16_t *in, uint16_t *out, int64_t batch, int64_t stride,
+                                     int lg_h, const WPrime &wp, cudaStream_t s) {
+  derivative_direct_kernel<<<grid_for(batch << lg_h), 256, 0, s>>>(in, out, batch, stride, lg_h, wp);
   return cudaGetLastError();
 }
 

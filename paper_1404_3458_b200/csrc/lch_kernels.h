@@ -186,6 +186,13 @@ cudaError_t launch_expand_rows(const uint16_t *comp, int64_t comp_stride, const 
 cudaError_t launch_expand_packets(const uint16_t *comp, int64_t comp_pos, const int32_t *rank,
                                   int64_t rank_stride, uint16_t *full, int64_t n, int64_t pkt, int64_t groups,
                                   cudaStream_t s);
+struct WPrime {
+  uint32_t w[16];  // W'_l (derivative.py:80-82)
+  int r;
+  uint32_t poly;
+};
+cudaError_t launch_derivative_direct(const uint16_t *in, uint16_t *out, int64_t batch, int64_t stride,
+                                     int lg_h, const WPrime &wp, cudaStream_t s);
 cudaError_t launch_pointwise_mul(const uint16_t *a, const uint16_t *b, uint16_t *out, int64_t count,
                                  const uint16_t *log, const uint16_t *exp, uint32_t m, cudaStream_t s);
 cudaError_t launch_stripes_to_packets(const uint8_t *bytes, int64_t len, int w, int64_t k, int64_t S,

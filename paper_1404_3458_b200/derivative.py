@@ -2,8 +2,8 @@
 derivative.py:1-82), executed on the GPU: scale by B_i, gather-XOR over the
 zero bits of j, scale by B_j^-1.
 
-derivative_direct (derivative.py:26-43) produces identical output by
-definition, so it is served by the same kernel path.
+derivative_direct (derivative.py:26-43) runs the direct per-coefficient
+formula in its own kernel (lch_derivative_direct), an independent path.
 """
 
 from __future__ import annotations
@@ -49,7 +49,16 @@ def derivative_fast(bt: BasisTables, coeffs: CoeffVec,
 
 
 def derivative_direct(bt: BasisTables, coeffs: CoeffVec) -> CoeffVec:
-    return derivative_fast(bt, coeffs)
+    """out[j] = sum over clear bits l of j of W'_l * d[j + 2^l] (derivative.py:26-43)."""
+    d = list(coeffs.data)
+    h = len(d)
+    _check(bt, h)
+    _lib.require_cuda()
+    src = _lib.to_device_u16(d).view(1, h)
+    dst = _lib.torch_mod().empty_like(src)
+    _lib.check(_lib.lib.lch_derivative_direct(bt.ctx.handle, src.data_ptr(), dst.data_ptr(), 1, h,
+                                              h.bit_length() - 1, _lib.stream_ptr()), "derivative")
+    return CoeffVec([int(x) for x in _lib.to_host_u16(dst)[0]])
 
 
 def w_prime_const(bt: BasisTables, l: int) -> int:

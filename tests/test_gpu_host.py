@@ -161,3 +161,33 @@ def test_decode_host_edge_counts(lch, bt8, orc8, count):
     decode_host(cp, bt8, hrx, bitmask_from_positions(256, erased), out, 500)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(out.numpy().view(np.uint16), msg)
+
+
+def test_back_to_back_decode_host_calls_keep_their_staging(lch, bt16):
+    """Two decode_host calls on different buffers queued without a host sync
+    in between (the survivor-compaction path reuses the context's page-locked
+    staging slots): each must decode its own rows (lch_api.cu
+    host_pipeline)."""
+    import torch
+    from paper_1404_3458_b200._lib import bitmask_from_positions
+    from paper_1404_3458_b200.rs import decode_host, encode_host
+    n, k, B = 1 << 16, 1 << 15, 96
+    cp = lch.CodeParams(16, k)
+    mask = O.gen_erasures(21, n, n - k, 0, 1)[0].astype(bool)
+    bits = bitmask_from_positions(n, np.nonzero(mask)[0])
+    rxs, outs, msgs = [], [], []
+    for seed in (31, 32, 33):
+        msg = O.gen_symbols(seed, 16, 0, B, k)
+        hp = torch.empty((B, n - k), dtype=torch.int16, pin_memory=True)
+        encode_host(cp, bt16, pinned(msg), hp)
+        torch.cuda.synchronize()
+        rx = np.concatenate([msg, hp.numpy().view(np.uint16)], axis=1)
+        rx[:, mask] = 0
+        rxs.append(pinned(rx))
+        outs.append(torch.empty((B, k), dtype=torch.int16, pin_memory=True))
+        msgs.append(msg)
+    for hrx, out in zip(rxs, outs):
+        decode_host(cp, bt16, hrx, bits, out, 8)  # chunks of 8 rows: many staging slots in flight
+    torch.cuda.synchronize()
+    for out, msg in zip(outs, msgs):
+        np.testing.assert_array_equal(out.numpy().view(np.uint16), msg)

@@ -1,4 +1,6 @@
 // C ABI (include/lch.h): context, pass planner and the codec pipelines.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -53,7 +55,12 @@ namespace {
     if (rc_ != LCH_OK) return rc_; \
   } while (0)
 
-int cu(cudaError_t e) { return e == cudaSuccess ? LCH_OK : (e == cudaErrorMemoryAllocation ? LCH_ENOMEM : LCH_ECUDA); }
+int cu(cudaError_t e) {
+  if (e == cudaSuccess) return LCH_OK;
+  static const bool verbose = std::getenv("LCH_VERBOSE_ERRORS") != nullptr;
+  if (verbose) std::fprintf(stderr, "liblch: CUDA error %d: %s\n", int(e), cudaGetErrorString(e));
+  return e == cudaErrorMemoryAllocation ? LCH_ENOMEM : LCH_ECUDA;
+}
 
 template <class T>
 int upload(T *&dst, const std::vector<T> &src) {
@@ -296,6 +303,41 @@ RawIO make_raw(uint16_t *ptr, int64_t stride, int64_t pkt = 0, int64_t npos = 0,
   return io;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// TMA view of a row-major raw input for the pass kernel's raw tiles:
+// {8 symbols, chunks of 8 positions over [pos_lo, min(pos_hi, 2^lgH)), rows},
+// boxes {8, 1, 256}: one chunk of 256 rows, [row][16 B] in shared memory.  False (use the register path) unless 16-byte aligned.
+bool make_raw_tma(const RawIO &io, int64_t batch, int lgH, CUtensorMap *m) {
+  if (io.pkt || !io.vec || io.pos_lo % 8) return false;
+  const int64_t hi = std::min<int64_t>(io.pos_hi, int64_t(1) << lgH);
+  if (hi <= io.pos_lo || (hi - io.pos_lo) % 8 || batch <= 0 || batch >= (int64_t(1) << 31)) return false;
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  // dims ordered by stride: {symbol in chunk, chunk, row}
+  const cuuint64_t dims[3] = {8, cuuint64_t((hi - io.pos_lo) / 8), cuuint64_t(batch)};
+  const cuuint64_t strides[2] = {16, cuuint64_t(io.row_stride) * 2};
+  const cuuint32_t box[3] = {8, 1, 256};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, io.ptr, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int R, uint32_t POLY>
 int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, const RawIO *raw_in,
              const uint4 *bs_in, const RawIO *raw_out, uint4 *work, cudaStream_t s,
@@ -327,7 +369,14 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     const bool first = i == 0, last = i + 1 == plan.size();
     p.in_mode = (first && raw_in) ? IO_RAW : IO_BS;
     p.out_mode = (last && raw_out) ? IO_RAW : IO_BS;
-    if (p.in_mode == IO_RAW) p.raw_in = *raw_in;
+    if (p.in_mode == IO_RAW) {
+      p.raw_in = *raw_in;
+      // TMA raw tiles: R = 16, tile = the 32 positions 32t .. 32t+31
+      bool low5 = R == 16 && p.tpb == 5;
+      for (int m = 0; m < p.tpb; ++m) low5 = low5 && p.gbit[m] == m;
+      static const bool no_tma = std::getenv("LCH_NO_RAW_TMA") != nullptr;
+      p.raw_tma = (low5 && !no_tma && make_raw_tma(p.raw_in, batch, lgH, &p.tm_in)) ? 1 : 0;
+    }
     if (p.out_mode == IO_RAW) p.raw_out = *raw_out;
     p.bs_in = (first && bs_in) ? bs_in : work;
     p.bs_out = work;
@@ -386,6 +435,8 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
     p.lwpc = 0;
     while (p.lwpc < 5 && (need(grp.size()) << (p.lwpc + 1)) <= GATHER_SMEM_MAX && (p.nbits + p.lwpc) < 10)
       ++p.lwpc;
+    // chunk-major blocks: one lane-word per CTA would read half sectors
+    if (p.lwpc == 0 && (need(grp.size()) << 1) <= GATHER_SMEM_CAP) p.lwpc = 1;
     p.lgH_in = lgH_in;
     p.lgH_out = lgH_out;
     std::vector<int> tile_and_special = grp;

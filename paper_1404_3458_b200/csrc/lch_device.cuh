@@ -280,6 +280,96 @@ struct GF {
     }
   }
 
+  // Compact forms of mul_acc_n2 / mul_acc2_n2: a rolled loop over 4 bits of f
+  // per iteration (two nested 2-bit digits), so a multiply is ~100
+  // instructions of code instead of ~450 (instruction-cache footprint of the
+  // pass kernel); p = x^t v is the only loop-carried state.
+  __device__ __forceinline__ static void digit_acc(uint32_t (&u)[R], const uint32_t (&p)[R],
+                                                   const uint32_t (&q)[R], uint32_t d) {
+    if (d & 1u) {
+      if (d & 2u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] = lop3_xor(u[b], p[b], q[b]);
+      } else {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] ^= p[b];
+      }
+    } else if (d & 2u) {
+#pragma unroll
+      for (int b = 0; b < R; ++b) u[b] ^= q[b];
+    }
+  }
+  __device__ __forceinline__ static void mul_acc_l(uint32_t (&u)[R], const uint32_t (&v)[R], uint32_t f) {
+    uint32_t p[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) p[b] = v[b];
+#pragma unroll 1
+    for (int t = 0; t < R; t += 4) {
+      uint32_t q[R], p2[R], q2[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) q[b] = xor_set(p, s1(b));
+      digit_acc(u, p, q, (f >> t) & 3u);
+#pragma unroll
+      for (int b = 0; b < R; ++b) p2[b] = xor_set(q, s1(b));
+#pragma unroll
+      for (int b = 0; b < R; ++b) q2[b] = xor_set(p2, s1(b));
+      digit_acc(u, p2, q2, (f >> (t + 2)) & 3u);
+#pragma unroll
+      for (int b = 0; b < R; ++b) p[b] = xor_set(q2, s1(b));
+    }
+  }
+  __device__ __forceinline__ static void digit_acc2(uint32_t (&u0)[R], const uint32_t (&p0)[R],
+                                                    const uint32_t (&q0)[R], uint32_t (&u1)[R],
+                                                    const uint32_t (&p1)[R], const uint32_t (&q1)[R],
+                                                    uint32_t d) {
+    if (d & 1u) {
+      if (d & 2u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] = lop3_xor(u0[b], p0[b], q0[b]);
+          u1[b] = lop3_xor(u1[b], p1[b], q1[b]);
+        }
+      } else {
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          u0[b] ^= p0[b];
+          u1[b] ^= p1[b];
+        }
+      }
+    } else if (d & 2u) {
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        u0[b] ^= q0[b];
+        u1[b] ^= q1[b];
+      }
+    }
+  }
+  __device__ __forceinline__ static void mul_acc2_l(uint32_t (&u0)[R], const uint32_t (&v0)[R],
+                                                    uint32_t (&u1)[R], const uint32_t (&v1)[R],
+                                                    uint32_t f) {
+    uint32_t p0[R], p1[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) {
+      p0[b] = v0[b];
+      p1[b] = v1[b];
+    }
+#pragma unroll 1
+    for (int t = 0; t < R; t += 2) {
+      uint32_t q0[R], q1[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        q0[b] = xor_set(p0, s1(b));
+        q1[b] = xor_set(p1, s1(b));
+      }
+      digit_acc2(u0, p0, q0, u1, p1, q1, (f >> t) & 3u);
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        p0[b] = xor_set(q0, s1(b));
+        p1[b] = xor_set(q1, s1(b));
+      }
+    }
+  }
+
 #ifndef LCH_MUL_2BIT
   // 1-bit digits: one warp-uniform branch per bit of f (fewer taken
   // branches than the 2-bit digits below: measured 4-5% faster passes)

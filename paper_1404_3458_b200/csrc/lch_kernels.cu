@@ -26,17 +26,15 @@ namespace lch {
 
 namespace {
 
-// Per-position block of the BS layout: 32 lanes x R plane-words, stored as
-// R/4 16-byte chunks per lane with a lane-dependent chunk swizzle so that
-// 128-bit shared-memory accesses by 8 consecutive lanes hit distinct banks.
+// Per-position block of the BS layout: 32 lanes x R plane-words, stored
+// chunk-major: 16-byte chunk c (planes 4c..4c+3) of lane w at c * 32 + w, so a
+// warp's 128-bit access to one chunk covers 512 contiguous bytes (shared
+// memory: conflict-free; global memory: fully coalesced).
 template <int R>
 struct Blk {
   static constexpr int CH = R / 4;
-  static constexpr int SWS = (CH == 4) ? 1 : 2;
   static constexpr int U4 = 8 * R;  // uint4 per position block
-  __device__ __forceinline__ static int chunk(int lane, int c) {
-    return lane * CH + (c ^ ((lane >> SWS) & (CH - 1)));
-  }
+  __device__ __forceinline__ static int chunk(int lane, int c) { return c * 32 + lane; }
   __device__ __forceinline__ static void load(const uint4 *blk, int lane, uint32_t (&v)[R]) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
@@ -61,6 +59,12 @@ struct Blk {
 #pragma unroll
     for (int c = 0; c < CH; ++c)
       blk[chunk(lane, c)] = make_uint4(v[4 * c + 0], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+  // straight from registers to global memory (streaming stores)
+  __device__ __forceinline__ static void store_g(uint4 *blk, int lane, const uint32_t (&v)[R]) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      __stcs(blk + chunk(lane, c), make_uint4(v[4 * c + 0], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
   }
 };
 
@@ -119,6 +123,18 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, unsigned
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ void cp_async16(void *smem_ptr, const void *gptr) {
@@ -200,6 +216,21 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
     return;
   }
   if (PDBG(9)) return;
+  if (R == 16 && p.raw_tma) {
+    // one thread: 4 chunks x 4 row blocks of 256, 64 KB, zero-filled outside
+    // the input (rows >= batch, positions outside [pos_lo, pos_hi))
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(bar, 64u * 1024u);
+      const int c0 = int((int64_t(base) - p.raw_in.pos_lo) >> 3);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb)
+          tma_load_3d(smem + c * 1024 + rb * 256, &p.tm_in, 0, c0 + c, g * GROUP + rb * 256, bar);
+    }
+    return;
+  }
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
   const int WPR = TP >> 1;
   const int64_t row0 = int64_t(g) * GROUP;
@@ -275,6 +306,41 @@ __device__ __forceinline__ void finish_tile_raw(uint4 *smem, int TP) {
     Blk<R>::store(bs + (2 * cw) * Blk<R>::U4, lane, lo);
     Blk<R>::store(bs + (2 * cw + 1) * Blk<R>::U4, lane, hi);
   }
+}
+
+// TMA-staged raw tile ([chunk c][row][16 B], c = positions 8c..8c+7) ->
+// bit-sliced tile, in place: chunk c's 16 KB are exactly the BS blocks of
+// positions 8c..8c+7.  Warps 2c, 2c+1 own chunk c; each reads two 32-bit
+// words (4 positions) of every row, then both sync and write back.
+template <int R>
+__device__ __forceinline__ void finish_tile_raw_tma(uint4 *smem) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = warp >> 1, wp = (warp & 1) * 2;
+  const uint32_t *reg = reinterpret_cast<const uint32_t *>(smem) + c * 4096 + wp;
+  uint32_t a[32], b[32];
+#pragma unroll
+  for (int L = 0; L < 32; ++L) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(reg + (32 * L + lane) * 4);
+    a[L] = v.x;
+    b[L] = v.y;
+  }
+  named_sync(1 + c, 64);
+  transpose32(a);
+  transpose32(b);
+  uint32_t x[R];
+  uint4 *bs = smem + (8 * c + 2 * wp) * Blk<R>::U4;
+#pragma unroll
+  for (int k = 0; k < R; ++k) x[k] = a[k];
+  Blk<R>::store(bs, lane, x);
+#pragma unroll
+  for (int k = 0; k < R; ++k) x[k] = a[16 + k];
+  Blk<R>::store(bs + Blk<R>::U4, lane, x);
+#pragma unroll
+  for (int k = 0; k < R; ++k) x[k] = b[k];
+  Blk<R>::store(bs + 2 * Blk<R>::U4, lane, x);
+#pragma unroll
+  for (int k = 0; k < R; ++k) x[k] = b[16 + k];
+  Blk<R>::store(bs + 3 * Blk<R>::U4, lane, x);
 }
 
 template <int R>
@@ -481,6 +547,8 @@ __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], ui
     F::mul_acc_lazy(u, v, f);
 #elif defined(LCH_MUL_LAZY2)
     F::mul_acc_lazy2(u, v, f);
+#elif defined(LCH_MUL_LOOP)
+    F::mul_acc_l(u, v, f);
 #elif defined(LCH_MUL_1BIT)
     F::mul_acc_1(u, v, f);
 #elif !defined(LCH_MUL_2BIT)
@@ -502,7 +570,9 @@ __device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R],
     F::xor_into(v1, u1);
   }
   if (f) {
-#if defined(LCH_MUL_1BIT)
+#if defined(LCH_MUL_LOOP)
+    F::mul_acc2_l(u0, v0, u1, v1, f);
+#elif defined(LCH_MUL_1BIT)
     F::mul_acc2_1(u0, v0, u1, v1, f);
 #elif !defined(LCH_MUL_2BIT)
     F::mul_acc2_n2(u0, v0, u1, v1, f);
@@ -565,7 +635,8 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   constexpr int PAT = (V >> 4) & 3;
   constexpr bool ROWONLY = V & 128;  // raw I/O in row layout only (no packet paths)
   constexpr int U4 = Blk<R>::U4;
-  extern __shared__ uint4 smem[];
+  // 128-byte aligned: TMA tensor copies land here
+  extern __shared__ __align__(128) uint4 smem[];
   uint4 *const bsm = smem + bs_offset_u4<R>();
   __shared__ uint32_t tpos[1 << TPB_MAX];
   __shared__ uint32_t fac[2][MAXOPS * (1 << TPB_MAX)];
@@ -604,6 +675,8 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // tile blocks (one contiguous buffer)
+  auto blk = [&](int q) -> uint4 * { return bsm + q * U4; };
   issue_tile<R, !RIN, ROWONLY>(p, smem, tpos, g, base, TP, &bar);
   int fb = 0;  // factor-table buffer of the current tile
   {
@@ -611,7 +684,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     fl.fetch(p, tpos, base);
     fl.put(fac[0]);
   }
-  if (!RIN || p.in_mode == IO_BS) {
+  if (!RIN || p.in_mode == IO_BS || p.raw_tma) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
   }
@@ -627,7 +700,12 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
     if (RIN && p.in_mode == IO_RAW) {
-      if (!(PDBG(128))) finish_tile_raw<R>(smem, TP);
+      if (!(PDBG(128))) {
+        if (R == 16 && p.raw_tma)
+          finish_tile_raw_tma<R>(smem);
+        else
+          finish_tile_raw<R>(smem, TP);
+      }
       __syncthreads();
     }
     if (PRE_OK && p.npre) {
@@ -644,11 +722,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       const int q0 = rr.q0w[warp];
       uint32_t a0[R], a1[R], a2[R], a3[R];
       if (active && !(PDBG(32))) {
-        Blk<R>::load(bsm + q0 * U4, lane, a0);
-        Blk<R>::load(bsm + (q0 | M0) * U4, lane, a1);
+        Blk<R>::load(blk(q0), lane, a0);
+        Blk<R>::load(blk(q0 | M0), lane, a1);
         if (has1) {
-          Blk<R>::load(bsm + (q0 | M1) * U4, lane, a2);
-          Blk<R>::load(bsm + (q0 | M0 | M1) * U4, lane, a3);
+          Blk<R>::load(blk(q0 | M1), lane, a2);
+          Blk<R>::load(blk(q0 | M0 | M1), lane, a3);
         }
       }
       FactorLoader nfl;
@@ -688,10 +766,10 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           }
         }
         if (!last_reg && !(PDBG(32))) {
-          Blk<R>::store(bsm + q0 * U4, lane, a0);
-          Blk<R>::store(bsm + (q0 | M0) * U4, lane, a1);
-          Blk<R>::store(bsm + (q0 | M1) * U4, lane, a2);
-          Blk<R>::store(bsm + (q0 | M0 | M1) * U4, lane, a3);
+          Blk<R>::store(blk(q0), lane, a0);
+          Blk<R>::store(blk(q0 | M0), lane, a1);
+          Blk<R>::store(blk(q0 | M1), lane, a2);
+          Blk<R>::store(blk(q0 | M0 | M1), lane, a3);
         }
       } else if (!SHAPED && active) {
         // A round's ops are [along m0]* [along m1]*.  Along m0 the pairs are
@@ -727,36 +805,25 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           }
         }
         if (!last_reg) {
-          Blk<R>::store(bsm + q0 * U4, lane, a0);
-          Blk<R>::store(bsm + (q0 | M0) * U4, lane, a1);
+          Blk<R>::store(blk(q0), lane, a0);
+          Blk<R>::store(blk(q0 | M0), lane, a1);
           if (has1) {
-            Blk<R>::store(bsm + (q0 | M1) * U4, lane, a2);
-            Blk<R>::store(bsm + (q0 | M0 | M1) * U4, lane, a3);
+            Blk<R>::store(blk(q0 | M1), lane, a2);
+            Blk<R>::store(blk(q0 | M0 | M1), lane, a3);
           }
         }
       }
       if (last_reg) {
-        // Drain the tile with bulk stores through a private 4 KB staging area
-        // per warp (two positions at a time): only warp-level syncs, and the
-        // stores overlap the next tile's rounds.
-        uint4 *stg = smem + stage_offset_u4<R>() + warp * 2 * U4;
+        // The tile leaves straight from registers: coalesced 512-byte
+        // streaming stores per chunk (no staging, no wait on earlier stores),
+        // overlapping the next tile's rounds.
         uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
-        if (active) {
-          const int qs[4] = {q0, q0 | M0, q0 | M1, q0 | M0 | M1};
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !has1) break;
-            if (lane == 0) tma_store_wait_read();  // this warp's previous bulk stores read their data
-            __syncwarp();
-            Blk<R>::store(stg, lane, h ? a2 : a0);
-            Blk<R>::store(stg + U4, lane, h ? a3 : a1);
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0 && !(PDBG(5))) {
-              tma_store_1d(dst + size_t(base | tpos[qs[2 * h]]) * U4, stg, U4 * 16);
-              tma_store_1d(dst + size_t(base | tpos[qs[2 * h + 1]]) * U4, stg + U4, U4 * 16);
-              tma_store_commit();
-            }
+        if (active && !(PDBG(5))) {
+          Blk<R>::store_g(dst + size_t(base | tpos[q0]) * U4, lane, a0);
+          Blk<R>::store_g(dst + size_t(base | tpos[q0 | M0]) * U4, lane, a1);
+          if (has1) {
+            Blk<R>::store_g(dst + size_t(base | tpos[q0 | M1]) * U4, lane, a2);
+            Blk<R>::store_g(dst + size_t(base | tpos[q0 | M0 | M1]) * U4, lane, a3);
           }
         }
         if (has_next && !(PDBG(64))) nfl.put(fac[fb ^ 1]);
@@ -807,7 +874,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       if (lane == 0) tma_store_wait_all();
       break;
     }
-    if (!RIN || p.in_mode == IO_BS) {
+    if (!RIN || p.in_mode == IO_BS || p.raw_tma) {
       mbar_wait(&bar, phase);
       phase ^= 1u;
     }
@@ -1397,9 +1464,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
 template <int R, uint32_t POLY>
 cudaError_t launch_gather(const GatherParams &p, int ngroups, cudaStream_t s) {
   const size_t smem = gather_smem_bytes(R, p);
-  if (smem > GATHER_SMEM_MAX) return cudaErrorInvalidValue;
+  if (smem > GATHER_SMEM_CAP) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> done{0};
-  cudaError_t e = smem_optin(gather_kernel<R, POLY>, int(GATHER_SMEM_MAX), done);
+  cudaError_t e = smem_optin(gather_kernel<R, POLY>, int(GATHER_SMEM_CAP), done);
   if (e != cudaSuccess) return e;
   dim3 grid(unsigned(ngroups) * (32u >> p.lwpc), 1u << (p.lgH_in - p.nbits));
   gather_kernel<R, POLY><<<grid, GNT, smem, s>>>(p);

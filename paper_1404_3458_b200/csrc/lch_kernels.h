@@ -1,6 +1,7 @@
 // Kernel parameter blocks and launchers (device side in lch_kernels.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -74,6 +75,12 @@ struct RawIO {
 };
 
 struct PassParams {
+  // raw_tma: the raw input tiles arrive by TMA through tm_in, a 3-D view
+  // {8 symbols (16 B), 16-byte chunks, rows} of the row-major input, as
+  // chunk-major [chunk][row][16 B] shared-memory tiles (R = 16, row layout,
+  // tile = positions 32t .. 32t+31)
+  alignas(64) CUtensorMap tm_in;
+  int raw_tma;
   int nops;
   PassOp ops[MAXOPS];
   int nrounds;
@@ -110,6 +117,9 @@ struct PassParams {
 // for j < 2^lgH_out.  One CTA per (tile, group, lane-word).
 constexpr int GMAXB = 11;
 constexpr size_t GATHER_SMEM_MAX = 96 * 1024;  // 2 CTAs per SM
+// largest tile (1 CTA per SM): two lane-words per CTA, so every 16-byte chunk
+// read shares its 32-byte sector with the neighbouring lane-word's
+constexpr size_t GATHER_SMEM_CAP = 200 * 1024;
 struct GatherParams {
   int nbits;
   int bits[GMAXB];

@@ -60,6 +60,12 @@ const char *lch_strerror(int code);
  * basis.build_basis_tables (basis.py:135-137) and walsh._fwht_of_log
  * (walsh.py:64-74).  max_h = 2^max_lg_h (<= 2^r). */
 int lch_init(int r, uint32_t poly, int max_lg_h, lch_ctx **out);
+/* As lch_init with the log/exp tables built from the generator alpha (an
+ * element index, FieldParams.alpha_index, field.py:31-49); LCH_ENOTPRIM when
+ * alpha does not generate GF(2^r)*.  lch_init uses alpha = 2 (the polynomial
+ * x).  Any primitive reduction polynomial is accepted; the two reference
+ * defaults run specialised kernels, others the runtime-taps instances. */
+int lch_init_alpha(int r, uint32_t poly, uint32_t alpha, int max_lg_h, lch_ctx **out);
 void lch_destroy(lch_ctx *ctx);
 
 /* Host copies of the tables (any pointer may be NULL).  Sizes: log[2^r],

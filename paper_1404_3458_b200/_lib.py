@@ -43,6 +43,7 @@ def _load() -> ctypes.CDLL:
         "lch_version": ([], ctypes.c_char_p),
         "lch_strerror": ([i32], ctypes.c_char_p),
         "lch_init": ([i32, u32, i32, ctypes.POINTER(P)], i32),
+        "lch_init_alpha": ([i32, u32, u32, i32, ctypes.POINTER(P)], i32),
         "lch_destroy": ([P], None),
         "lch_get_tables": ([P] + [P] * 9, i32),
         "lch_forward": ([P, P, i64, i64, i32, u32, i64, P], i32),
@@ -99,11 +100,11 @@ def check(rc: int, what: str = "") -> None:
 class Context:
     """One liblch context: tables for (r, poly) with capacity 2^max_lg_h."""
 
-    def __init__(self, r: int, poly: int, max_lg_h: int):
+    def __init__(self, r: int, poly: int, max_lg_h: int, alpha: int = 2):
         h = ctypes.c_void_p()
-        check(lib.lch_init(r, poly, max_lg_h, ctypes.byref(h)), "lch_init")
+        check(lib.lch_init_alpha(r, poly, alpha, max_lg_h, ctypes.byref(h)), "lch_init")
         self.handle = h
-        self.r, self.poly, self.max_lg_h = r, poly, max_lg_h
+        self.r, self.poly, self.max_lg_h, self.alpha = r, poly, max_lg_h, alpha
         self.lock = threading.Lock()
 
     def __del__(self):

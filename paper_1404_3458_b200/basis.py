@@ -24,7 +24,7 @@ class BasisTables:
         self.max_h = max_h
         self.levels = max_h.bit_length() - 1
         r = ft.r
-        self.ctx = _lib.Context(r, ft.params.reduction_poly, self.levels)
+        self.ctx = _lib.Context(r, ft.params.reduction_poly, self.levels, ft.params.alpha_index)
         t = self.ctx.tables()
         self._np = t
         self.w_on_basis: list[list[int]] = [[int(x) for x in row] for row in t["w_on_basis"]]

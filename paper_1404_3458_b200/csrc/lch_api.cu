@@ -381,6 +381,7 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
     p.bs_in = (first && bs_in) ? bs_in : work;
     p.bs_out = work;
     p.w_hat = c->d_w_hat;
+    p.taps = c->t.poly & (c->t.order - 1u);
     if (last && gt_out) {
       p.gt_out = gt_out;
       p.gt_lgH = gt_lgH;
@@ -428,6 +429,7 @@ int run_gather(lch_ctx *c, const uint4 *y, uint4 *t, int lgH_in, int lgH_out, in
   for (auto grp : groups) {
     GatherParams p;
     std::memset(&p, 0, sizeof(p));
+    p.taps = c->t.poly & (c->t.order - 1u);
     p.sb = (first && special >= 0) ? special : -1;
     p.c = cconst;
     p.nbits = int(grp.size());
@@ -461,7 +463,9 @@ int dispatch(lch_ctx *c, Fn &&fn) {
     return fn(std::integral_constant<int, 16>{}, std::integral_constant<uint32_t, 0x1100Bu>{});
   if (c->t.r == 8 && c->t.poly == 0x11Du)
     return fn(std::integral_constant<int, 8>{}, std::integral_constant<uint32_t, 0x11Du>{});
-  return LCH_EUNSUPPORTED;
+  // any other primitive polynomial: the runtime-taps instances
+  if (c->t.r == 16) return fn(std::integral_constant<int, 16>{}, std::integral_constant<uint32_t, 0u>{});
+  return fn(std::integral_constant<int, 8>{}, std::integral_constant<uint32_t, 0u>{});
 }
 
 uint32_t hs_of(const lch_ctx *c, int level, uint32_t shift) {
@@ -485,7 +489,7 @@ int locator_impl(lch_ctx *c, const uint32_t *bits, int64_t np, uint16_t *loc_out
                                 reinterpret_cast<uintptr_t>(epi->phi) % 16 == 0 && epi->rx_stride % 8 == 0);
   // one CTA per pattern: used when there are enough patterns to fill the GPU
   // (a single pattern runs faster as 4 grid-wide radix-2^8 passes)
-  if (r == 16 && aligned && np >= 32) {
+  if (r == 16 && c->t.poly == 0x1100Bu && aligned && np >= 32) {
     FwhtParams p;
     std::memset(&p, 0, sizeof(p));
     p.nvec = np;
@@ -570,12 +574,16 @@ const char *lch_strerror(int code) {
 }
 
 int lch_init(int r, uint32_t poly, int max_lg_h, lch_ctx **out) {
+  return lch_init_alpha(r, poly, 2u, max_lg_h, out);
+}
+
+int lch_init_alpha(int r, uint32_t poly, uint32_t alpha, int max_lg_h, lch_ctx **out) {
   if (!out) return LCH_EINVAL;
   *out = nullptr;
   if (max_lg_h < 0 || max_lg_h > 16) return LCH_EINVAL;
   lch_ctx *c = new (std::nothrow) lch_ctx();
   if (!c) return LCH_ENOMEM;
-  int rc = build_tables(r, poly, 1u << max_lg_h, c->t);
+  int rc = build_tables(r, poly, 1u << max_lg_h, c->t, alpha);
   if (rc != LCH_OK) {
     delete c;
     return rc;

@@ -521,6 +521,47 @@ struct GF {
   }
 };
 
+// The same multiplies for a reduction polynomial known only at run time (any
+// primitive polynomial, field.py:28-53): taps in a warp-uniform register, so
+// x * p costs one masked XOR per plane instead of one XOR per tap.
+template <int R>
+struct GFrt {
+  uint32_t taps;  // POLY & (2^R - 1)
+  __device__ __forceinline__ void step(const uint32_t (&p)[R], uint32_t (&q)[R]) const {
+    const uint32_t top = p[R - 1];
+#pragma unroll
+    for (int b = 0; b < R; ++b) q[b] = (b ? p[b > 0 ? b - 1 : 0] : 0u) ^ (top & (0u - ((taps >> b) & 1u)));
+  }
+  __device__ __forceinline__ void mul_acc(uint32_t (&u)[R], const uint32_t (&v)[R], uint32_t f) const {
+    uint32_t p[R];
+#pragma unroll
+    for (int b = 0; b < R; ++b) p[b] = v[b];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      if ((f >> t) & 1u) {
+#pragma unroll
+        for (int b = 0; b < R; ++b) u[b] ^= p[b];
+      }
+      if (t + 1 < R) {
+        uint32_t q[R];
+        step(p, q);
+#pragma unroll
+        for (int b = 0; b < R; ++b) p[b] = q[b];
+      }
+    }
+  }
+  __device__ __forceinline__ void mul_acc2(uint32_t (&u0)[R], const uint32_t (&v0)[R], uint32_t (&u1)[R],
+                                           const uint32_t (&v1)[R], uint32_t f) const {
+    mul_acc(u0, v0, f);
+    mul_acc(u1, v1, f);
+  }
+  __device__ __forceinline__ void mul(uint32_t (&acc)[R], const uint32_t (&v)[R], uint32_t f) const {
+#pragma unroll
+    for (int b = 0; b < R; ++b) acc[b] = 0u;
+    mul_acc(acc, v, f);
+  }
+};
+
 // Product of two GF(2^16) symbols (polynomial basis, x^16 + x^12 + x^3 + x + 1,
 // field.py:100-129) without tables.  gf16_clmul: the carry-less 16x16
 // product from 9 integer multiplies of bit-interleaved thirds (the bits of a

@@ -509,40 +509,13 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
 
 }  // namespace
 
+// Multiplier: the compile-time-polynomial GF<R, POLY>, or (POLY == 0) the
+// runtime-taps GFrt<R> for any other primitive polynomial.
 template <int R, uint32_t POLY>
-__device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *smem,
-                                            const uint32_t *tpos, uint32_t base, int TP,
-                                            int64_t trow) {
-  using F = GF<R, POLY>;
-  constexpr int U4 = Blk<R>::U4;
-  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
-  for (int q = warp; q < TP; q += NWARP) {
-    uint32_t v[R];
-    Blk<R>::load(smem + q * U4, lane, v);
-    for (int o = 0; o < nops; ++o) {
-      const uint32_t f = __shfl_sync(
-          0xffffffffu, uint32_t(__ldg(ops[o].table + trow * ops[o].tab_stride + (base | tpos[q]))), 0);
-      uint32_t acc[R];
-#pragma unroll
-      for (int b = 0; b < R; ++b) acc[b] = 0u;
-      if (f) F::mul_acc_n2(acc, v, f);
-#pragma unroll
-      for (int b = 0; b < R; ++b) v[b] = acc[b];
-    }
-    Blk<R>::store(smem + q * U4, lane, v);
-  }
-}
-
-// One LCH butterfly on a pair of bit-sliced positions (u at the block's lower
-// half): forward transform.py:126-133 (u' = u + f v, v' = u' + v) or inverse
-// transform.py:165-169 (v' = u + v, u' = u + f v').  f is warp-uniform.
-template <int R, uint32_t POLY>
-__device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv) {
-  using F = GF<R, POLY>;
-  if (inv) F::xor_into(v, u);
-  // zero factors (block 0 of every level at shift 0, transform.py:154-161)
-  // are a warp-uniform skip
-  if (f) {
+struct Mul {
+  __device__ __forceinline__ explicit Mul(uint32_t) {}
+  __device__ __forceinline__ void acc(uint32_t (&u)[R], const uint32_t (&v)[R], uint32_t f) const {
+    using F = GF<R, POLY>;
 #if defined(LCH_MUL_LAZY)
     F::mul_acc_lazy(u, v, f);
 #elif defined(LCH_MUL_LAZY2)
@@ -557,19 +530,9 @@ __device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], ui
     F::mul_acc(u, v, f);
 #endif
   }
-  if (!inv) F::xor_into(v, u);
-}
-
-// Two butterflies sharing one factor (pairs (u0, v0) and (u1, v1)).
-template <int R, uint32_t POLY>
-__device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R], uint32_t (&u1)[R],
-                                           uint32_t (&v1)[R], uint32_t f, bool inv) {
-  using F = GF<R, POLY>;
-  if (inv) {
-    F::xor_into(v0, u0);
-    F::xor_into(v1, u1);
-  }
-  if (f) {
+  __device__ __forceinline__ void acc2(uint32_t (&u0)[R], const uint32_t (&v0)[R], uint32_t (&u1)[R],
+                                       const uint32_t (&v1)[R], uint32_t f) const {
+    using F = GF<R, POLY>;
 #if defined(LCH_MUL_LOOP)
     F::mul_acc2_l(u0, v0, u1, v1, f);
 #elif defined(LCH_MUL_1BIT)
@@ -580,6 +543,73 @@ __device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R],
     F::mul_acc2(u0, v0, u1, v1, f);
 #endif
   }
+  __device__ __forceinline__ void mul(uint32_t (&a)[R], const uint32_t (&v)[R], uint32_t f) const {
+    GF<R, POLY>::mul(a, v, f);
+  }
+};
+template <int R>
+struct Mul<R, 0u> {
+  GFrt<R> g;
+  __device__ __forceinline__ explicit Mul(uint32_t taps) : g{taps} {}
+  __device__ __forceinline__ void acc(uint32_t (&u)[R], const uint32_t (&v)[R], uint32_t f) const {
+    g.mul_acc(u, v, f);
+  }
+  __device__ __forceinline__ void acc2(uint32_t (&u0)[R], const uint32_t (&v0)[R], uint32_t (&u1)[R],
+                                       const uint32_t (&v1)[R], uint32_t f) const {
+    g.mul_acc2(u0, v0, u1, v1, f);
+  }
+  __device__ __forceinline__ void mul(uint32_t (&a)[R], const uint32_t (&v)[R], uint32_t f) const {
+    g.mul(a, v, f);
+  }
+};
+
+template <int R, uint32_t POLY>
+__device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *smem,
+                                            const uint32_t *tpos, uint32_t base, int TP,
+                                            int64_t trow, const Mul<R, POLY> &mm) {
+  constexpr int U4 = Blk<R>::U4;
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
+  for (int q = warp; q < TP; q += NWARP) {
+    uint32_t v[R];
+    Blk<R>::load(smem + q * U4, lane, v);
+    for (int o = 0; o < nops; ++o) {
+      const uint32_t f = __shfl_sync(
+          0xffffffffu, uint32_t(__ldg(ops[o].table + trow * ops[o].tab_stride + (base | tpos[q]))), 0);
+      uint32_t acc[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] = 0u;
+      if (f) mm.acc(acc, v, f);
+#pragma unroll
+      for (int b = 0; b < R; ++b) v[b] = acc[b];
+    }
+    Blk<R>::store(smem + q * U4, lane, v);
+  }
+}
+
+// One LCH butterfly on a pair of bit-sliced positions (u at the block's lower
+// half): forward transform.py:126-133 (u' = u + f v, v' = u' + v) or inverse
+// transform.py:165-169 (v' = u + v, u' = u + f v').  f is warp-uniform.
+template <int R, uint32_t POLY>
+__device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv,
+                                          const Mul<R, POLY> &mm) {
+  using F = GF<R, 16u>;  // xor_into only (polynomial-independent)
+  if (inv) F::xor_into(v, u);
+  // zero factors (block 0 of every level at shift 0, transform.py:154-161)
+  // are a warp-uniform skip
+  if (f) mm.acc(u, v, f);
+  if (!inv) F::xor_into(v, u);
+}
+
+// Two butterflies sharing one factor (pairs (u0, v0) and (u1, v1)).
+template <int R, uint32_t POLY>
+__device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R], uint32_t (&u1)[R],
+                                           uint32_t (&v1)[R], uint32_t f, bool inv, const Mul<R, POLY> &mm) {
+  using F = GF<R, 16u>;
+  if (inv) {
+    F::xor_into(v0, u0);
+    F::xor_into(v1, u1);
+  }
+  if (f) mm.acc2(u0, v0, u1, v1, f);
   if (!inv) {
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);
@@ -642,6 +672,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   __shared__ uint32_t fac[2][MAXOPS * (1 << TPB_MAX)];
   __shared__ __align__(8) uint64_t bar;
   unsigned phase = 0;
+  const Mul<R, POLY> mm(__shfl_sync(0xffffffffu, p.taps, 0));
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through a shuffle: provably warp-uniform for the compiler, so
   // the butterfly factors and their digit tests live in uniform registers
@@ -709,7 +740,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
       __syncthreads();
     }
     if (PRE_OK && p.npre) {
-      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
+      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0, mm);
       __syncthreads();
     }
     for (int rd = 0; rd < p.nrounds; ++rd) {
@@ -746,11 +777,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
         const uint32_t fa = __shfl_sync(0xffffffffu, ft[q0], 0);
         const bool inv_a = PAT == 2 ? false : oa.kind == OP_INV;
         if (PAT ? PAT == 2 : oa.shared) {
-          butterfly2<R, POLY>(a0, a1, a2, a3, fa, inv_a);
+          butterfly2<R, POLY>(a0, a1, a2, a3, fa, inv_a, mm);
         } else {
           const uint32_t fa2 = __shfl_sync(0xffffffffu, ft[q0 | M1], 0);
-          butterfly<R, POLY>(a0, a1, fa, inv_a);
-          butterfly<R, POLY>(a2, a3, fa2, inv_a);
+          butterfly<R, POLY>(a0, a1, fa, inv_a, mm);
+          butterfly<R, POLY>(a2, a3, fa2, inv_a, mm);
         }
         if (rr.shape == 2) {
           const uint32_t *fu = ft + (1 << TPB_MAX);
@@ -758,11 +789,11 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           const uint32_t fb1 = __shfl_sync(0xffffffffu, fu[q0], 0);
           const bool inv_b = PAT == 2 ? false : ob.kind == OP_INV;
           if (PAT ? PAT == 1 : ob.shared) {
-            butterfly2<R, POLY>(a0, a2, a1, a3, fb1, inv_b);
+            butterfly2<R, POLY>(a0, a2, a1, a3, fb1, inv_b, mm);
           } else {
             const uint32_t fb2 = __shfl_sync(0xffffffffu, fu[q0 | M0], 0);
-            butterfly<R, POLY>(a0, a2, fb1, inv_b);
-            butterfly<R, POLY>(a1, a3, fb2, inv_b);
+            butterfly<R, POLY>(a0, a2, fb1, inv_b, mm);
+            butterfly<R, POLY>(a1, a3, fb2, inv_b, mm);
           }
         }
         if (!last_reg && !(PDBG(32))) {
@@ -790,10 +821,10 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           }
           const uint32_t *ft = fac[fb] + o * (1 << TPB_MAX);
           const uint32_t f1 = __shfl_sync(0xffffffffu, ft[q0], 0);
-          butterfly<R, POLY>(a0, a1, f1, inv);
+          butterfly<R, POLY>(a0, a1, f1, inv, mm);
           if (has1) {
             const uint32_t f2 = __shfl_sync(0xffffffffu, ft[sw ? (q0 | M0) : (q0 | M1)], 0);
-            butterfly<R, POLY>(a2, a3, f2, inv);
+            butterfly<R, POLY>(a2, a3, f2, inv, mm);
           }
         }
         if (sw) {
@@ -832,7 +863,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
     }
     if (!reg_path) {
       if (POST_OK && p.npost) {
-        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0);
+        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0, mm);
         __syncthreads();
       }
       if (POST_OK && p.gt_out) {
@@ -927,9 +958,15 @@ cudaError_t launch_pass_v(const PassParams &p, unsigned ctas, size_t smem, cudaS
 #if LCH_PASS_TU == 0 || LCH_PASS_TU == 7
 template cudaError_t launch_pass_v<8, 0x11Du, LCH_PASS_TU>(const PassParams &, unsigned, size_t, cudaStream_t);
 #endif
+#if LCH_PASS_TU == 7  // any other primitive polynomial (taps at run time)
+template cudaError_t launch_pass_v<8, 0u, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
+template cudaError_t launch_pass_v<16, 0u, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
+#endif
 template cudaError_t launch_pass_v<16, 0x1100Bu, LCH_PASS_TU>(const PassParams &, unsigned, size_t,
                                                                 cudaStream_t);
 #else  // the main unit: every kernel but the pass instances
+extern template cudaError_t launch_pass_v<8, 0u, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0u, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<8, 0x11Du, 0>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<8, 0x11Du, 7>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 0>(const PassParams &, unsigned, size_t, cudaStream_t);
@@ -1051,7 +1088,7 @@ __global__ void __launch_bounds__(GNT, 2) gather_kernel(const __grid_constant__ 
       ld(ytile, e, x);
 #pragma unroll
       for (int b = 0; b < R; ++b) z[b] ^= x[b];
-      GF<R, POLY>::mul(cz, z, p.c);  // c is a kernel constant: uniform
+      Mul<R, POLY>(p.taps).mul(cz, z, p.c);  // c is a kernel constant: uniform
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= cz[b];
     }
@@ -1426,7 +1463,10 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
   const size_t smem = pass_smem_bytes(R, p.tpb, raw);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
   const unsigned ctas = unsigned(std::min<int64_t>(total, int64_t(2) * sm_count()));
-  if constexpr (R == 16) {
+  if constexpr (POLY == 0u) {  // runtime polynomial: one generic instance
+    (void)v;
+    return launch_pass_v<R, 0u, 7>(p, ctas, smem, s);
+  } else if constexpr (R == 16) {
     switch (v) {  // the instances the codec's passes use; everything else runs generic
       case 0: return launch_pass_v<R, POLY, 0>(p, ctas, smem, s);
       case 1: return launch_pass_v<R, POLY, 1>(p, ctas, smem, s);
@@ -1726,8 +1766,12 @@ cudaError_t launch_count_bits(const uint32_t *bits, int64_t npatterns, int words
 
 template cudaError_t launch_pass<16, 0x1100Bu>(const PassParams &, int, cudaStream_t);
 template cudaError_t launch_pass<8, 0x11Du>(const PassParams &, int, cudaStream_t);
+template cudaError_t launch_pass<16, 0u>(const PassParams &, int, cudaStream_t);
+template cudaError_t launch_pass<8, 0u>(const PassParams &, int, cudaStream_t);
 template cudaError_t launch_gather<16, 0x1100Bu>(const GatherParams &, int, cudaStream_t);
 template cudaError_t launch_gather<8, 0x11Du>(const GatherParams &, int, cudaStream_t);
+template cudaError_t launch_gather<16, 0u>(const GatherParams &, int, cudaStream_t);
+template cudaError_t launch_gather<8, 0u>(const GatherParams &, int, cudaStream_t);
 #endif  // LCH_PASS_TU
 
 }  // namespace lch

@@ -81,6 +81,7 @@ struct PassParams {
   // tile = positions 32t .. 32t+31)
   alignas(64) CUtensorMap tm_in;
   int raw_tma;
+  uint32_t taps;         // reduction polynomial & (2^R - 1) (runtime-polynomial instances)
   int nops;
   PassOp ops[MAXOPS];
   int nrounds;
@@ -121,6 +122,7 @@ constexpr size_t GATHER_SMEM_MAX = 96 * 1024;  // 2 CTAs per SM
 // read shares its 32-byte sector with the neighbouring lane-word's
 constexpr size_t GATHER_SMEM_CAP = 200 * 1024;
 struct GatherParams {
+  uint32_t taps;  // reduction polynomial & (2^R - 1) (runtime-polynomial instances)
   int nbits;
   int bits[GMAXB];
   int sb;                // the special (top) position bit, not a tile bit, or -1

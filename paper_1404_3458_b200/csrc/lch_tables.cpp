@@ -39,21 +39,24 @@ void fwht_host(std::vector<uint32_t> &a, uint32_t mod) {
       }
 }
 
-int build_tables(int r, uint32_t poly, uint32_t max_h, Tables &t) {
+int build_tables(int r, uint32_t poly, uint32_t max_h, Tables &t, uint32_t alpha) {
   if (r != 8 && r != 16) return LCH_EINVAL;               // field.py:42-43
   if ((poly >> r) != 1u) return LCH_EINVAL;               // degree check, field.py:44-47
   if (max_h < 1 || (max_h & (max_h - 1)) || max_h > (1u << r)) return LCH_EINVAL;  // basis.py:35-38
+  if (alpha == 0 || alpha >= (1u << r)) return LCH_EINVAL;                            // field.py:48-49
 
   t.r = r;
   t.poly = poly;
+  t.alpha = alpha;
   t.order = 1u << r;
   t.m = t.order - 1;
   t.max_h = max_h;
   t.levels = 0;
   while ((1u << t.levels) < max_h) ++t.levels;
 
-  // log/exp: walk the powers of alpha = x; a repeat before 2^r - 1 steps (or
-  // not returning to 1) means the polynomial is not primitive.
+  // log/exp: walk the powers of alpha (x by default); a repeat before 2^r - 1
+  // steps (or not returning to 1) means alpha does not generate the group
+  // (polynomial not primitive, or alpha not a generator; field.py:116-133).
   t.log.assign(t.order, 0);
   t.exp.assign(t.order, 0);
   std::vector<uint8_t> seen(t.order, 0);
@@ -63,7 +66,7 @@ int build_tables(int r, uint32_t poly, uint32_t max_h, Tables &t) {
     seen[val] = 1;
     t.exp[e] = uint16_t(val);
     t.log[val] = uint16_t(e);
-    val = clmul_reduce(val, 2, poly, r);
+    val = clmul_reduce(val, alpha, poly, r);
   }
   if (val != 1) return LCH_ENOTPRIM;
   t.log[0] = 0;        // log(0) := 0 convention; zero operands are branched on

@@ -15,6 +15,7 @@ namespace lch {
 struct Tables {
   int r = 0;
   uint32_t poly = 0;
+  uint32_t alpha = 2;    // generator the log/exp tables are built from (field.py:31-39)
   uint32_t order = 0;   // 2^r
   uint32_t m = 0;       // 2^r - 1
   uint32_t max_h = 0;
@@ -41,7 +42,7 @@ struct Tables {
 };
 
 // Returns 0 or a negative LCH_E* code (lch.h).
-int build_tables(int r, uint32_t poly, uint32_t max_h, Tables &t);
+int build_tables(int r, uint32_t poly, uint32_t max_h, Tables &t, uint32_t alpha = 2);
 
 // In-place FWHT over Z_mod (host helper used for the cached FWHT(log)).
 void fwht_host(std::vector<uint32_t> &a, uint32_t mod);

@@ -354,6 +354,52 @@ def make_shards() -> None:
         json.dump(res, fh, indent=1)
 
 
+def make_fields() -> None:
+    """Non-default fields (SURVEY §8a field row; field.py:28-53): other
+    primitive reduction polynomials and other generators alpha.  Writes
+    golden_fields.json: table digests, transforms, encode / decode outputs."""
+    from binfec.field import FieldParams, build_tables
+    from binfec.rs import CodeParams, ErasurePattern
+    cases = []
+    for r, poly, alpha, k in ((8, 0x12B, 2, 128), (8, 0x11D, 19, 128), (8, 0x163, 2, 32),
+                              (16, 0x1002D, 2, 1 << 15), (16, 0x1100B, 3, 1 << 15)):
+        ft = build_tables(FieldParams(r, poly, alpha))
+        n = 1 << r
+        bt = build_basis_tables(ft, n)
+        seed = 1404345900 + r + alpha
+        c = {"r": r, "poly": poly, "alpha": alpha, "k": k, "seed": seed,
+             "log": digest(np.asarray(ft.log, np.uint16)), "exp": digest(np.asarray(ft.exp, np.uint16)),
+             "w_hat": digest(np.asarray([x for lvl in bt.w_hat for x in lvl], np.uint16)),
+             "b_prod": digest(np.asarray(bt.b_prod, np.uint16))}
+        a = gen_symbols(seed, r, 0, n)
+        c["forward_shift0"] = {"sha256": digest(forward(bt, CoeffVec(a), 0).data)}
+        c["inverse_shift0"] = {"sha256": digest(inverse(bt, EvalVec(a, 0)).data)}
+        h = n // 4
+        c["forward_h4_shift"] = {"h": h, "shift": 3 * h,
+                                 "sha256": digest(forward(bt, CoeffVec(a[:h]), 3 * h).data)}
+        cp = CodeParams(r, k)
+        ncw = 4 if r == 8 else 1
+        enc, dec, junk_dec = [], [], []
+        for cw in range(ncw):
+            m = gen_symbols(seed + 1, r, cw, k)
+            sym = ref_rs.encode(cp, bt, m).symbols
+            enc.append(digest(sym[k:]))
+            er = gen_erasures(seed + 2, n, n - k, cw)
+            pat = ErasurePattern.of(n, er)
+            junk = gen_symbols(seed + 3, r, cw, n)
+            rx = [junk[j] if j in set(er) else sym[j] for j in range(n)]
+            out = ref_rs.decode(cp, bt, ft, rx, pat)
+            assert out == m
+            dec.append(digest(out))
+            junk_dec.append(digest(ref_rs.decode(cp, bt, ft, junk, pat)))
+        c["encode_parity"] = enc
+        c["decode_junk"] = junk_dec
+        cases.append(c)
+        print("fields", r, hex(poly), alpha, flush=True)
+    with open(os.path.join(HERE, "golden_fields.json"), "w") as fh:
+        json.dump(cases, fh, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["r8", "r16"]
     if "r8" in which:
@@ -365,6 +411,9 @@ if __name__ == "__main__":
     if "r16" in which or "r16_anyk" in which:
         make_r16_anyk()
         print("r16_anyk done", flush=True)
+    if "fields" in which:
+        make_fields()
+        print("fields done", flush=True)
     if "shards" in which or which == ["r8", "r16"]:
         make_shards()
         print("shards done", flush=True)

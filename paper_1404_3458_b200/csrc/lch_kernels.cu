@@ -401,6 +401,50 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
       *reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, bb, j0))) = a;
       *reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, bb, j0 + 1))) = b;
     }
+  } else if (!io.pkt && io.vec && TP == 32 && inwin && io.merge_src && !io.pinv_log) {
+    // survivors merged from merge_src (decode, rs.py:140-148): each thread's
+    // 16 row chunks in four batches of 4, all 4 survivor loads in flight before
+    // any is consumed (a load per chunk would wait a full memory round trip
+    // each: the stores below may alias merge_src for the compiler)
+    constexpr int NBATCH = 4, HALF_ITEMS = (GROUP * 4) / NT / NBATCH;
+#pragma unroll 1
+    for (int h = 0; h < NBATCH; ++h) {
+      uint4 src[HALF_ITEMS];
+      uint32_t ebs[HALF_ITEMS];
+#pragma unroll
+      for (int i = 0; i < HALF_ITEMS; ++i) {
+        const int idx = tid + (h * HALF_ITEMS + i) * NT;
+        const int r = idx >> 2, c = idx & 3;
+        const int64_t b = row0 + r;
+        const uint32_t pos0 = base + 8 * c;
+        uint32_t eb = 0xFFu;
+        if (b < p.batch) eb = (io.merge_bits[b * io.bits_stride + (pos0 >> 5)] >> (pos0 & 31)) & 0xFFu;
+        ebs[i] = eb;
+        src[i] = eb != 0xFFu ? __ldg(reinterpret_cast<const uint4 *>(io.merge_src + b * io.merge_stride + pos0))
+                             : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int i = 0; i < HALF_ITEMS; ++i) {
+        const int idx = tid + (h * HALF_ITEMS + i) * NT;
+        const int r = idx >> 2, c = idx & 3;
+        const int64_t b = row0 + r;
+        if (b >= p.batch) continue;
+        uint4 val = make_uint4(rs[stage_idx(r, 4 * c + 0)], rs[stage_idx(r, 4 * c + 1)],
+                               rs[stage_idx(r, 4 * c + 2)], rs[stage_idx(r, 4 * c + 3)]);
+        const uint32_t eb = ebs[i];
+        if (eb != 0xFFu) {
+          uint32_t *vv = &val.x;
+          const uint32_t *ss = &src[i].x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t keep_lo = (eb >> (2 * q)) & 1u, keep_hi = (eb >> (2 * q + 1)) & 1u;
+            const uint32_t msk = (keep_lo ? 0x0000FFFFu : 0u) | (keep_hi ? 0xFFFF0000u : 0u);
+            vv[q] = (vv[q] & msk) | (ss[q] & ~msk);
+          }
+        }
+        reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, b, base)))[c] = val;
+      }
+    }
   } else if (!io.pkt && io.vec && TP >= 8 && inwin) {
     const int lcpr = p.tpb - 3;
     for (int idx = tid; idx < (GROUP << lcpr); idx += NT) {

@@ -71,3 +71,56 @@ def test_split_range_covers_total():
     with pytest.raises(ValueError):
         from paper_1404_3458_b200.dist import shard_range
         shard_range(2, 2, 4)
+
+
+def _bench_worker(rank, world, port, out):
+    """bench.py's own rank plumbing (the functions run_codec / run_stripe use):
+    shard ownership, seeded per-shard inputs, a per-rank step time reduced
+    with max_over_ranks, per-rank values gathered to rank 0."""
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from oracle import oracle as O
+
+    r, w, _ = bench.env_rank()
+    lo, hi = bench.codeword_shard(r, w, 2)  # 2 codewords per rank (weak scaling)
+    glo, ghi = bench.group_shard(r, w, 21)  # 21 stripe groups over the ranks (strong scaling)
+    msgs = O.gen_symbols(bench.SEED_MSG, 8, lo, hi - lo, 128)
+    par = O.Oracle(8).encode_batch(128, msgs, 1)
+    step_ms = 1.0 + 0.25 * r  # the slowest rank defines the job
+    mx = bench.max_over_ranks([step_ms])[0]
+    per = bench.gather_to_rank0({"rank": r, "cw": (lo, hi), "groups": (glo, ghi), "ms": step_ms,
+                                 "msgs": msgs.tolist(), "par": par.tolist(), "max": mx})
+    if r == 0:
+        out.put(per)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_eight_rank_bench_plumbing_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    W = 8
+    procs = [ctx.Process(target=_bench_worker, args=(r, W, port, q)) for r in range(W)]
+    for p in procs:
+        p.start()
+    per = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert [d["rank"] for d in per] == list(range(W))
+    cws = [d["cw"] for d in per]
+    assert cws[0][0] == 0 and all(a[1] == b[0] for a, b in zip(cws, cws[1:])) and cws[-1][1] == 2 * W
+    grs = [d["groups"] for d in per]
+    assert grs[0][0] == 0 and all(a[1] == b[0] for a, b in zip(grs, grs[1:])) and grs[-1][1] == 21
+    assert all(d["max"] == 1.0 + 0.25 * (W - 1) for d in per)  # max over ranks, on every rank
+    from oracle import oracle as O
+    import bench
+    full = O.gen_symbols(bench.SEED_MSG, 8, 0, 2 * W, 128)
+    np.testing.assert_array_equal(np.asarray(sum((d["msgs"] for d in per), []), np.uint16), full)
+    np.testing.assert_array_equal(np.asarray(sum((d["par"] for d in per), []), np.uint16),
+                                  O.Oracle(8).encode_batch(128, full, 4))

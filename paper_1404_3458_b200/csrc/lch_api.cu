@@ -377,7 +377,20 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
       static const bool no_tma = std::getenv("LCH_NO_RAW_TMA") != nullptr;
       p.raw_tma = (low5 && !no_tma && make_raw_tma(p.raw_in, batch, lgH, &p.tm_in)) ? 1 : 0;
     }
-    if (p.out_mode == IO_RAW) p.raw_out = *raw_out;
+    if (p.out_mode == IO_RAW) {
+      p.raw_out = *raw_out;
+      // prefetch of the merge's survivor chunks (decode output tiles of 32
+      // positions starting at position 0; the merge source indexed by
+      // absolute position)
+      const RawIO &o = p.raw_out;
+      bool low5 = R == 16 && p.tpb == 5 && o.pkt == 0 && o.pos_lo == 0 && o.merge_src && !o.pinv_log;
+      for (int m = 0; m < p.tpb; ++m) low5 = low5 && p.gbit[m] == m;
+      static const bool no_tma = std::getenv("LCH_NO_RAW_TMA") != nullptr;
+      if (low5 && !no_tma) {
+        RawIO ms = make_raw(const_cast<uint16_t *>(o.merge_src), o.merge_stride, 0, 0, 0, o.pos_hi);
+        p.merge_tma = make_raw_tma(ms, batch, lgH, &p.tm_merge) ? 1 : 0;
+      }
+    }
     p.bs_in = (first && bs_in) ? bs_in : work;
     p.bs_out = work;
     p.w_hat = c->d_w_hat;

@@ -420,8 +420,11 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
         uint32_t eb = 0xFFu;
         if (b < p.batch) eb = (io.merge_bits[b * io.bits_stride + (pos0 >> 5)] >> (pos0 & 31)) & 0xFFu;
         ebs[i] = eb;
-        src[i] = eb != 0xFFu ? __ldg(reinterpret_cast<const uint4 *>(io.merge_src + b * io.merge_stride + pos0))
-                             : make_uint4(0u, 0u, 0u, 0u);
+        if (p.merge_tma && c < 2)  // prefetched by TMA into the spare area: [chunk][row][16 B]
+          src[i] = smem[stage_offset_u4<R>() + c * GROUP + r];
+        else
+          src[i] = eb != 0xFFu ? __ldg(reinterpret_cast<const uint4 *>(io.merge_src + b * io.merge_stride + pos0))
+                               : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
       for (int i = 0; i < HALF_ITEMS; ++i) {
@@ -714,8 +717,8 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   uint4 *const bsm = smem + bs_offset_u4<R>();
   __shared__ uint32_t tpos[1 << TPB_MAX];
   __shared__ uint32_t fac[2][MAXOPS * (1 << TPB_MAX)];
-  __shared__ __align__(8) uint64_t bar;
-  unsigned phase = 0;
+  __shared__ __align__(8) uint64_t bar, bar_m;
+  unsigned phase = 0, phase_m = 0;
   const Mul<R, POLY> mm(__shfl_sync(0xffffffffu, p.taps, 0));
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through a shuffle: provably warp-uniform for the compiler, so
@@ -747,6 +750,7 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   uint32_t base = base_of(tl);
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&bar_m, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -774,6 +778,18 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
   for (;;) {
     const int next = tl + int(gridDim.x);
     const bool has_next = next < total;
+    if (ROUT && R == 16 && p.merge_tma && threadIdx.x == 0) {
+      // survivors of position chunks 0-1 of this tile, for the output merge
+      uint4 *dst = smem + stage_offset_u4<R>();
+      fence_proxy_async();
+      mbar_expect_tx(&bar_m, 32u * 1024u);
+      const int c0 = int(int64_t(base) >> 3);
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int rb = 0; rb < 4; ++rb)
+          tma_load_3d(dst + c * GROUP + rb * 256, &p.tm_merge, 0, c0 + c, g * GROUP + rb * 256, &bar_m);
+    }
     if (RIN && p.in_mode == IO_RAW) {
       if (!(PDBG(128))) {
         if (R == 16 && p.raw_tma)
@@ -930,10 +946,15 @@ __global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ Pas
           Blk<R>::store(gdst + size_t(pos) * U4, lane, acc);
         }
       }
-      if (!ROUT || p.out_mode == IO_BS)
+      if (!ROUT || p.out_mode == IO_BS) {
         store_tile_bs<R>(p, bsm, tpos, g, base, TP);
-      else
+      } else {
+        if (R == 16 && p.merge_tma) {
+          mbar_wait(&bar_m, phase_m);
+          phase_m ^= 1u;
+        }
         store_tile_raw<R, ROWONLY>(p, smem, g, base, TP);
+      }
       __syncthreads();
       if (has_next) {
         const uint32_t nb = base_of(next);

@@ -80,7 +80,11 @@ struct PassParams {
   // chunk-major [chunk][row][16 B] shared-memory tiles (R = 16, row layout,
   // tile = positions 32t .. 32t+31)
   alignas(64) CUtensorMap tm_in;
-  int raw_tma;
+  // merge_tma: the decode's survivor source (raw_out.merge_src) for position
+  // chunks 0-1 of each output tile arrives by TMA (tm_merge, same view as
+  // tm_in) into the spare 32 KB of shared memory while the tile computes
+  alignas(64) CUtensorMap tm_merge;
+  int raw_tma, merge_tma;
   uint32_t taps;         // reduction polynomial & (2^R - 1) (runtime-polynomial instances)
   int nops;
   PassOp ops[MAXOPS];

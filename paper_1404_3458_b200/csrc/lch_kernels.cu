@@ -703,7 +703,13 @@ struct FactorLoader {
 // compiled out, which keeps the hot loop's code footprint small (the pure
 // butterfly passes run 5-7 % faster in the V = 0 instance).
 template <int R, uint32_t POLY, int V>
-__global__ void __launch_bounds__(NT, 2) pass_kernel(const __grid_constant__ PassParams p) {
+// 2 CTAs per SM (128 registers: 4 positions x 16 planes + the multiply's
+// chain).  Measured: 3 CTAs at 80 registers made the pure butterfly passes
+// 24-28 % slower (V = 24: 165 -> 204 us), spills in the others.
+#ifndef LCH_PASS_MINB
+#define LCH_PASS_MINB(V) 2
+#endif
+__global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid_constant__ PassParams p) {
   constexpr bool RIN = V & 1, ROUT = V & 2, EXTRA = V & 4, SHAPED = V & 8;
   // bit 6: scalings before the rounds only; bit 8: after them (and the gather epilogue) only
   constexpr bool PRE_OK = EXTRA && !(V & 256), POST_OK = EXTRA && !(V & 64);
@@ -1015,7 +1021,20 @@ cudaError_t launch_pass_v(const PassParams &p, unsigned ctas, size_t smem, cudaS
   static std::atomic<uint64_t> done{0};
   cudaError_t e = smem_optin(pass_kernel<R, POLY, V>, int(pass_smem_bytes(R, TPB_MAX, true)), done);
   if (e != cudaSuccess) return e;
-  pass_kernel<R, POLY, V><<<ctas, NT, smem, s>>>(p);
+  // persistent CTAs: as many as fit on the device (2 or 3 per SM)
+  static std::atomic<int> occ_cache[2] = {{0}, {0}};
+  std::atomic<int> &oc = occ_cache[smem > pass_smem_bytes(R, TPB_MAX, false) ? 1 : 0];
+  int occ = oc.load(std::memory_order_relaxed);
+  if (occ <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<R, POLY, V>, NT, smem) != cudaSuccess ||
+        occ <= 0) {
+      cudaGetLastError();
+      occ = 2;
+    }
+    oc.store(occ, std::memory_order_relaxed);
+  }
+  const unsigned maxc = unsigned(occ) * unsigned(sm_count());
+  pass_kernel<R, POLY, V><<<std::min(ctas, maxc), NT, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1478,18 +1497,18 @@ __global__ void count_bits_kernel(const uint32_t *bits, int64_t npatterns, int w
 
 // ---------------------------------------------------------------------------
 
-size_t pass_smem_bytes(int R, int tpb, bool raw) {
-  // [raw staging (R = 8 only)] [BS tile] [half-tile bulk-store staging]
+size_t pass_smem_bytes(int R, int tpb, bool stage) {
+  // [raw staging (R = 8 only)] [BS tile] [half-tile area: the decode merge's
+  // prefetched survivors (raw-output passes only, R = 16)]
   (void)tpb;
-  (void)raw;
   const size_t tile = (size_t(1) << TPB_MAX) * 8 * R * 16;
   const size_t pre = R == 16 ? 0 : size_t(GROUP) * (size_t(1) << TPB_MAX) * 2;
-  return pre + tile + tile / 2;
+  return pre + tile + ((stage || R != 16) ? tile / 2 : 0);
 }
 
 template <int R, uint32_t POLY>
 cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
-  const bool raw = p.in_mode == IO_RAW || p.out_mode == IO_RAW;
+  (void)0;
   int v = (p.in_mode == IO_RAW ? 1 : 0) | (p.out_mode == IO_RAW ? 2 : 0) |
           ((p.npre || p.npost || p.gt_out) ? 4 : 0);
   bool shaped = p.nrounds > 0;
@@ -1525,9 +1544,9 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
     if (vs == 221 || vs == 108 || vs == 284 || vs == 430) v = vs;
   }
   if (std::getenv("LCH_NO_LEAN")) v = 7;
-  const size_t smem = pass_smem_bytes(R, p.tpb, raw);
+  const size_t smem = pass_smem_bytes(R, p.tpb, p.out_mode == IO_RAW);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
-  const unsigned ctas = unsigned(std::min<int64_t>(total, int64_t(2) * sm_count()));
+  const unsigned ctas = unsigned(std::min<int64_t>(total, int64_t(4) * sm_count()));
   if constexpr (POLY == 0u) {  // runtime polynomial: one generic instance
     (void)v;
     return launch_pass_v<R, 0u, 7>(p, ctas, smem, s);

@@ -4,6 +4,7 @@
 //   V=0: mul_acc_n2 (nested 2-bit digits, two uniform branches per digit)
 //   V=1: 2-bit digits through a 4-way switch
 //   V=2: 3-bit windows (p, x p, x^2 p live) through an 8-way switch
+//   V=3: 1-bit digits, predicated XORs (no branches)
 // nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/mulbench2.cu -o tools/mulbench2_bin
 #include <cstdint>
 #include <cstdio>
@@ -90,11 +91,43 @@ __device__ __forceinline__ void mul_w3(uint32_t (&u)[R], const uint32_t (&v)[R],
   }
 }
 
+
+// predicated accumulation: u ^= p under a (warp-uniform) predicate, 16 planes
+// in one asm block so the predicate is set once (no branches at all)
+__device__ __forceinline__ void pxor16(uint32_t (&u)[R], const uint32_t (&p)[R], uint32_t cond) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %32, 0;\n"
+      "@q xor.b32 %0, %0, %16;\n @q xor.b32 %1, %1, %17;\n @q xor.b32 %2, %2, %18;\n @q xor.b32 %3, %3, %19;\n"
+      "@q xor.b32 %4, %4, %20;\n @q xor.b32 %5, %5, %21;\n @q xor.b32 %6, %6, %22;\n @q xor.b32 %7, %7, %23;\n"
+      "@q xor.b32 %8, %8, %24;\n @q xor.b32 %9, %9, %25;\n @q xor.b32 %10, %10, %26;\n @q xor.b32 %11, %11, %27;\n"
+      "@q xor.b32 %12, %12, %28;\n @q xor.b32 %13, %13, %29;\n @q xor.b32 %14, %14, %30;\n @q xor.b32 %15, %15, %31;\n}"
+      : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
+        "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15])
+      : "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7]),
+        "r"(p[8]), "r"(p[9]), "r"(p[10]), "r"(p[11]), "r"(p[12]), "r"(p[13]), "r"(p[14]), "r"(p[15]), "r"(cond));
+}
+
+__device__ __forceinline__ void mul_pred(uint32_t (&u)[R], const uint32_t (&v)[R], uint32_t f) {
+  uint32_t p[R];
+#pragma unroll
+  for (int b = 0; b < R; ++b) p[b] = v[b];
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    pxor16(u, p, (f >> t) & 1u);
+    if (t + 1 < R) {
+      uint32_t q[R];
+      adv(p, q);
+#pragma unroll
+      for (int b = 0; b < R; ++b) p[b] = q[b];
+    }
+  }
+}
+
 template <int V>
 __device__ __forceinline__ void mac(uint32_t (&u)[R], const uint32_t (&v)[R], uint32_t f) {
   if (V == 0) F::mul_acc_n2(u, v, f);
   else if (V == 1) mul_sw2(u, v, f);
-  else mul_w3(u, v, f);
+  else if (V == 2) mul_w3(u, v, f);
+  else mul_pred(u, v, f);
 }
 
 template <int V>
@@ -139,15 +172,16 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int iters = 1000;
-  uint32_t ref[3] = {0, 0, 0};
-  for (int V = 0; V < 3; ++V) {
+  uint32_t ref[4] = {0, 0, 0, 0};
+  for (int V = 0; V < 4; ++V) {
     const int grid = 148 * 2;
     float ms = 0;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
       if (V == 0) k<0><<<grid, 256>>>(fac, out, iters);
       else if (V == 1) k<1><<<grid, 256>>>(fac, out, iters);
-      else k<2><<<grid, 256>>>(fac, out, iters);
+      else if (V == 2) k<2><<<grid, 256>>>(fac, out, iters);
+      else k<3><<<grid, 256>>>(fac, out, iters);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms, a, b);
@@ -159,6 +193,6 @@ int main() {
     printf("V=%d 16 warps/SM: %.3f ms  %.3f T symbol-butterflies/s  check %08x (%s)\n", V, ms, bf / ms / 1e9,
            ref[V], cudaGetErrorString(cudaGetLastError()));
   }
-  printf(ref[0] == ref[1] && ref[1] == ref[2] ? "variants agree\n" : "VARIANTS DIFFER\n");
+  printf(ref[0] == ref[1] && ref[1] == ref[2] && ref[2] == ref[3] ? "variants agree\n" : "VARIANTS DIFFER\n");
   return 0;
 }

@@ -401,6 +401,57 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
       *reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, bb, j0))) = a;
       *reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, bb, j0 + 1))) = b;
     }
+  } else if (R == 16 && !io.pkt && io.vec && TP == 32 && inwin && io.merge_src && io.pinv_log && io.pinv_val &&
+             ((io.pinv_stride & 7) | (reinterpret_cast<uintptr_t>(io.pinv_log) & 15)) == 0) {
+    // per-codeword patterns (rs.decode row by row): erased j < k get the
+    // computed value times 1 / Pi'(row, j) (table-free products), survivors
+    // are copied from merge_src; each thread's 16 row chunks in batches of 4
+    // with all their loads (bitmask word, 1 / Pi' and survivor chunks) in
+    // flight before any is consumed
+    constexpr int NB = 4, PER = (GROUP * 4) / NT / NB;
+#pragma unroll 1
+    for (int h = 0; h < NB; ++h) {
+      uint4 src[PER], pw[PER];
+      uint32_t ebs[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int idx = tid + (h * PER + i) * NT;
+        const int r = idx >> 2, c = idx & 3;
+        const int64_t b = row0 + r;
+        const uint32_t pos0 = base + 8 * c;
+        uint32_t eb = 0u;
+        if (b < p.batch) eb = (io.merge_bits[b * io.bits_stride + (pos0 >> 5)] >> (pos0 & 31)) & 0xFFu;
+        ebs[i] = eb;
+        const bool ok = b < p.batch;
+        src[i] = ok && eb != 0xFFu
+                     ? __ldg(reinterpret_cast<const uint4 *>(io.merge_src + b * io.merge_stride + pos0))
+                     : make_uint4(0u, 0u, 0u, 0u);
+        pw[i] = ok && eb ? __ldg(reinterpret_cast<const uint4 *>(io.pinv_log + b * io.pinv_stride + pos0))
+                         : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        const int idx = tid + (h * PER + i) * NT;
+        const int r = idx >> 2, c = idx & 3;
+        const int64_t b = row0 + r;
+        if (b >= p.batch) continue;
+        uint4 val = make_uint4(rs[stage_idx(r, 4 * c + 0)], rs[stage_idx(r, 4 * c + 1)],
+                               rs[stage_idx(r, 4 * c + 2)], rs[stage_idx(r, 4 * c + 3)]);
+        uint32_t *vv = &val.x;
+        const uint32_t *ss = &src[i].x, *pp = &pw[i].x;
+        const uint32_t eb = ebs[i];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w = vv[q];
+          if ((eb >> (2 * q)) & 1u) w = (w & 0xFFFF0000u) | gf16_mul(w & 0xFFFFu, pp[q] & 0xFFFFu);
+          else w = (w & 0xFFFF0000u) | (ss[q] & 0xFFFFu);
+          if ((eb >> (2 * q + 1)) & 1u) w = (w & 0xFFFFu) | (gf16_mul(w >> 16, pp[q] >> 16) << 16);
+          else w = (w & 0xFFFFu) | (ss[q] & 0xFFFF0000u);
+          vv[q] = w;
+        }
+        reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, b, base)))[c] = val;
+      }
+    }
   } else if (!io.pkt && io.vec && TP == 32 && inwin && io.merge_src && !io.pinv_log) {
     // survivors merged from merge_src (decode, rs.py:140-148): each thread's
     // 16 row chunks in four batches of 4, all 4 survivor loads in flight before

@@ -357,7 +357,7 @@ __device__ __forceinline__ void column_to_words(const uint4 *bs, int cw, int lan
 }
 
 template <int R, bool ROWONLY = false>
-__device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem, int g,
+__device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem, int g, const uint32_t *red,
                                                uint32_t base, int TP) {
   if (PDBG(5)) return;
   if (int64_t(base) + TP <= p.raw_out.pos_lo || int64_t(base) >= p.raw_out.pos_hi) return;
@@ -443,9 +443,9 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t w = vv[q];
-          if ((eb >> (2 * q)) & 1u) w = (w & 0xFFFF0000u) | gf16_mul(w & 0xFFFFu, pp[q] & 0xFFFFu);
+          if ((eb >> (2 * q)) & 1u) w = (w & 0xFFFF0000u) | gf16_mul_t(w & 0xFFFFu, pp[q] & 0xFFFFu, red);
           else w = (w & 0xFFFF0000u) | (ss[q] & 0xFFFFu);
-          if ((eb >> (2 * q + 1)) & 1u) w = (w & 0xFFFFu) | (gf16_mul(w >> 16, pp[q] >> 16) << 16);
+          if ((eb >> (2 * q + 1)) & 1u) w = (w & 0xFFFFu) | (gf16_mul_t(w >> 16, pp[q] >> 16, red) << 16);
           else w = (w & 0xFFFFu) | (ss[q] & 0xFFFF0000u);
           vv[q] = w;
         }
@@ -775,6 +775,9 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
   __shared__ uint32_t tpos[1 << TPB_MAX];
   __shared__ uint32_t fac[2][MAXOPS * (1 << TPB_MAX)];
   __shared__ __align__(8) uint64_t bar, bar_m;
+  // (raw-output instances) (x << 16) mod p / (x << 24) mod p for the
+  // per-codeword division by Pi' (gf16_mul_t): two lookups instead of folds
+  __shared__ uint32_t red16[(V & 2) && R == 16 ? 384 : 1];
   unsigned phase = 0, phase_m = 0;
   const Mul<R, POLY> mm(__shfl_sync(0xffffffffu, p.taps, 0));
   const int tid = threadIdx.x, lane = tid & 31;
@@ -805,6 +808,10 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
   };
   int g = tl >> p.lgnt;
   uint32_t base = base_of(tl);
+  if constexpr ((V & 2) && R == 16) {
+    if (POLY == 0x1100Bu)
+      for (int i = tid; i < 384; i += NT) red16[i] = gf16_fold(i < 256 ? uint32_t(i) << 16 : uint32_t(i - 256) << 24);
+  }
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_init(&bar_m, 1);
@@ -1010,7 +1017,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
           mbar_wait(&bar_m, phase_m);
           phase_m ^= 1u;
         }
-        store_tile_raw<R, ROWONLY>(p, smem, g, base, TP);
+        store_tile_raw<R, ROWONLY>(p, smem, g, red16, base, TP);
       }
       __syncthreads();
       if (has_next) {

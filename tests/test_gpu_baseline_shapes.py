@@ -179,3 +179,35 @@ def test_cfg4b_per_codeword_decode_4096(lch, bt16, orc, cfg34):
     rows = sample_rows(4096, 12, 5)
     mh = masks[rows].cpu().numpy().astype(np.uint8)
     np.testing.assert_array_equal(host(out[rows]), orc.decode_batch(K, host(junk[rows]), mh, nthreads=NTH))
+
+
+def test_cfg2_transforms_1024_x_2_16(lch, bt16, orc):
+    """Config 2 exactly: 1024 polynomials, h = 2^16 (seed 1404345802):
+    forward (shift 0 and a nonzero shift), inverse, derivative; 16 sampled
+    polynomials against the oracle, full-batch round trips."""
+    import torch
+    from paper_1404_3458_b200 import gen
+    from paper_1404_3458_b200.derivative import run_derivative
+    from paper_1404_3458_b200.transform import run_transform
+    B = 1024
+    x = gen.symbols(bt16.ctx, 1404345802, 0, B, N)
+    xin = host(x)
+    rows = sample_rows(B, 16, 6)
+    for shift in (0, 40503):
+        y = x.clone()
+        run_transform(bt16, y, shift, False)
+        got = host(y[rows])
+        for i, r in enumerate(rows):
+            np.testing.assert_array_equal(got[i], orc.forward(xin[r], shift), err_msg=f"row {r}")
+        run_transform(bt16, y, shift, True)
+        torch.testing.assert_close(y, x, rtol=0, atol=0)
+    z = x.clone()
+    run_transform(bt16, z, 0, True)
+    got = host(z[rows])
+    for i, r in enumerate(rows):
+        np.testing.assert_array_equal(got[i], orc.inverse(xin[r], 0))
+    d = torch.empty_like(x)
+    run_derivative(bt16, x, d)
+    got = host(d[rows[:8]])
+    for i, r in enumerate(rows[:8]):
+        np.testing.assert_array_equal(got[i], orc.derivative(xin[r]))

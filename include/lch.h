@@ -141,11 +141,13 @@ int lch_decode(lch_ctx *ctx, const uint16_t *rx, int64_t row_stride_in,
  * The codeword is the evaluation at omega_0..omega_(n-1) of the unique
  * polynomial of degree < k through the message at omega_0..omega_(k-1)
  * (novel-basis interpolation).  For power-of-two k this is lch_encode
- * (rs.encode, rs.py:85-96); otherwise the parity is computed by erasure-
- * decoding E = [k, n) with the reference's decode algorithm (rs.py:125-148):
- * locator of E, Phi = msg * Pi_bar, n-point inverse, derivative, n-point
- * forward, division by Pi' on [k, n).  Layouts as lch_encode; in packet
- * layout the strides count positions per stripe group. */
+ * (rs.encode, rs.py:85-96); otherwise the default is a recursive systematic
+ * encoder over the binary expansion of k (fused power-of-two encode plans
+ * and XORs); LCH_ENCODE_BY_DECODE=1 selects the
+ * erasure-decode formulation instead (E = [k, n), the reference's decode
+ * algorithm rs.py:125-148; same codeword, kept as a cross-check).  Layouts
+ * as lch_encode; in packet layout the strides count positions per stripe
+ * group. */
 int lch_encode_k(lch_ctx *ctx, const uint16_t *msg, int64_t stride_in, uint16_t *parity,
                  int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len,
                  void *stream);

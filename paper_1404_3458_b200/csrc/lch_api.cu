@@ -376,6 +376,11 @@ int run_plan(lch_ctx *c, const std::vector<Plan> &plan, int lgH, int64_t batch, 
       for (int m = 0; m < p.tpb; ++m) low5 = low5 && p.gbit[m] == m;
       static const bool no_tma = std::getenv("LCH_NO_RAW_TMA") != nullptr;
       p.raw_tma = (low5 && !no_tma && make_raw_tma(p.raw_in, batch, lgH, &p.tm_in)) ? 1 : 0;
+      // packet layout: bulk copies of the 2 KB lane runs (window in whole tiles)
+      const RawIO &ri = p.raw_in;
+      p.raw_bulk = (low5 && !no_tma && ri.pkt >= GROUP && ri.pkt % GROUP == 0 && ri.pos_lo % 32 == 0 &&
+                    (std::min<int64_t>(ri.pos_hi, int64_t(1) << lgH) - ri.pos_lo) % 32 == 0 &&
+                    reinterpret_cast<uintptr_t>(ri.ptr) % 16 == 0) ? 1 : 0;
     }
     if (p.out_mode == IO_RAW) {
       p.raw_out = *raw_out;

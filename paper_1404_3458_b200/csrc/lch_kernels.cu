@@ -231,6 +231,29 @@ __device__ __forceinline__ void issue_tile(const PassParams &p, uint4 *smem, con
     }
     return;
   }
+  if (R == 16 && p.raw_bulk) {
+    // packet layout: 32 bulk copies of 2 KB (one per position, lane 0 of
+    // each warp issues 4); a tile outside the window arrives without bytes
+    // and is zeroed by finish_tile_raw_bulk
+    const RawIO &io = p.raw_in;
+    const bool in = int64_t(base) >= io.pos_lo && int64_t(base) < io.pos_hi;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+      fence_proxy_async();
+      if (w == 0) {
+        if (in)
+          mbar_expect_tx(bar, 64u * 1024u);
+        else
+          mbar_arrive(bar);
+      }
+      if (in) {
+        const int64_t row0 = int64_t(g) * GROUP;
+        for (int q = 4 * w; q < 4 * w + 4; ++q)
+          tma_load_1d(smem + q * 128, raw_addr(io, row0, int64_t(base) + q), 2048u, bar);
+      }
+    }
+    return;
+  }
   uint32_t *rs = reinterpret_cast<uint32_t *>(smem);
   const int WPR = TP >> 1;
   const int64_t row0 = int64_t(g) * GROUP;
@@ -341,6 +364,37 @@ __device__ __forceinline__ void finish_tile_raw_tma(uint4 *smem) {
 #pragma unroll
   for (int k = 0; k < R; ++k) x[k] = b[16 + k];
   Blk<R>::store(bs + 3 * Blk<R>::U4, lane, x);
+}
+
+// Bulk-staged packet tile ([position][1024 lanes] of uint16) -> bit-sliced
+// tile in place: warp w owns positions 4w .. 4w+3, two at a time (their 4 KB
+// of rows become their 4 KB of BS blocks), so only warp-level syncs.
+template <int R>
+__device__ __forceinline__ void finish_tile_raw_bulk(uint4 *smem, bool in) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint16_t *sv = reinterpret_cast<const uint16_t *>(smem);
+#pragma unroll 1
+  for (int pp = 0; pp < 2; ++pp) {
+    const int p0 = 4 * warp + 2 * pp;
+    uint32_t a[32];
+    if (in) {
+#pragma unroll
+      for (int L = 0; L < 32; ++L)
+        a[L] = uint32_t(sv[p0 * GROUP + 32 * L + lane]) | (uint32_t(sv[(p0 + 1) * GROUP + 32 * L + lane]) << 16);
+      __syncwarp();
+      transpose32(a);
+    } else {
+#pragma unroll
+      for (int L = 0; L < 32; ++L) a[L] = 0u;
+    }
+    uint32_t x[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[k] = a[k];
+    Blk<R>::store(smem + p0 * Blk<R>::U4, lane, x);
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[k] = a[16 + k];
+    Blk<R>::store(smem + (p0 + 1) * Blk<R>::U4, lane, x);
+  }
 }
 
 template <int R>
@@ -827,7 +881,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
     fl.fetch(p, tpos, base);
     fl.put(fac[0]);
   }
-  if (!RIN || p.in_mode == IO_BS || p.raw_tma) {
+  if (!RIN || p.in_mode == IO_BS || p.raw_tma || p.raw_bulk) {
     mbar_wait(&bar, phase);
     phase ^= 1u;
   }
@@ -858,6 +912,8 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
       if (!(PDBG(128))) {
         if (R == 16 && p.raw_tma)
           finish_tile_raw_tma<R>(smem);
+        else if (R == 16 && p.raw_bulk)
+          finish_tile_raw_bulk<R>(smem, int64_t(base) >= p.raw_in.pos_lo && int64_t(base) < p.raw_in.pos_hi);
         else
           finish_tile_raw<R>(smem, TP);
       }
@@ -1034,7 +1090,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
       if (lane == 0) tma_store_wait_all();
       break;
     }
-    if (!RIN || p.in_mode == IO_BS || p.raw_tma) {
+    if (!RIN || p.in_mode == IO_BS || p.raw_tma || p.raw_bulk) {
       mbar_wait(&bar, phase);
       phase ^= 1u;
     }

@@ -85,6 +85,10 @@ struct PassParams {
   // tm_in) into the spare 32 KB of shared memory while the tile computes
   alignas(64) CUtensorMap tm_merge;
   int raw_tma, merge_tma;
+  // raw_bulk: packet-layout raw input tiles (R = 16, tile = 32 consecutive
+  // positions, window aligned to 32): each position's 1024 lanes are one
+  // contiguous 2 KB run, fetched by a 1-D bulk copy into [position][lane]
+  int raw_bulk;
   uint32_t taps;         // reduction polynomial & (2^R - 1) (runtime-polynomial instances)
   int nops;
   PassOp ops[MAXOPS];

@@ -167,9 +167,16 @@ int lch_decode_k(lch_ctx *ctx, const uint16_t *rx, int64_t stride_in,
  * batch streams through the GPU in chunks of `chunk` rows (codewords, or
  * stripe groups when packet_len > 0; 0 = ~64 MiB per chunk): host->device
  * copies, kernels and device->host copies of neighbouring chunks overlap on
- * three streams.  Ordered on `stream` like the device entry points.  Layouts
- * and semantics as lch_encode_k / lch_decode_k; erasure counts are taken
- * from the host bitmasks (no device round trip). */
+ * three streams.  The kernels and the OUTPUT buffers are ordered on `stream`
+ * like the device entry points.  Host INPUT buffers must hold their data when
+ * the call is made (like the arrays handed to the reference's BatchCodec):
+ * their copies start right away, so they overlap the tail of an earlier call
+ * still in flight on the same context (the device slots and page-locked
+ * staging persist in the context; lch_release_host_buffers frees them).
+ * lch_set_host_ordering(ctx, 1) restores stream-ordered reads of the inputs
+ * (for callers that fill them by earlier work on `stream`).  Layouts and
+ * semantics as lch_encode_k / lch_decode_k; erasure counts are taken from the
+ * host bitmasks (no device round trip). */
 int lch_encode_host(lch_ctx *ctx, const uint16_t *host_msg, int64_t stride_in,
                     uint16_t *host_parity, int64_t stride_out, int64_t batch, int64_t k,
                     int64_t packet_len, int64_t chunk, void *stream);
@@ -177,6 +184,14 @@ int lch_decode_host(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride_in,
                     const uint32_t *host_bits, int shared, uint16_t *host_out,
                     int64_t stride_out, int64_t batch, int64_t k, int64_t packet_len,
                     int64_t chunk, void *stream);
+
+/* stream_ordered != 0: the host-buffer entry points read their host inputs in
+ * stream order (after the work already queued on `stream`); 0 (default): at
+ * the call. */
+int lch_set_host_ordering(lch_ctx *ctx, int stream_ordered);
+/* Waits for the device and frees the pipeline's persistent device slots and
+ * page-locked staging buffers (they are re-created on demand). */
+int lch_release_host_buffers(lch_ctx *ctx);
 
 /* Host helper of the decode pipeline: row r of host_out = the survivors
  * (bit j of host_bits clear) of row r of host_rx, in order (multi-threaded,

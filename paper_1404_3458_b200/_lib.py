@@ -56,6 +56,8 @@ def _load() -> ctypes.CDLL:
         "lch_encode_k": ([P, P, i64, P, i64, i64, i64, i64, P], i32),
         "lch_decode_k": ([P, P, i64, P, i32, P, i64, i64, i64, i64, P, P], i32),
         "lch_set_scratch_limit": ([P, u64], i32),
+        "lch_set_host_ordering": ([P, i32], i32),
+        "lch_release_host_buffers": ([P], i32),
         "lch_compact_rows": ([P, P, i64, P, i64, i64, P, i64], i32),
         "lch_encode_host": ([P, P, i64, P, i64, i64, i64, i64, i64, P], i32),
         "lch_decode_host": ([P, P, i64, P, i32, P, i64, i64, i64, i64, i64, P], i32),

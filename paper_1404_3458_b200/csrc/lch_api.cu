@@ -9,6 +9,7 @@
 #include <cstring>
 #include <functional>
 #include <memory>
+#include <string>
 #include <thread>
 #include <mutex>
 #include <type_traits>
@@ -42,6 +43,15 @@ struct lch_ctx {
   // it before refilling the slot, also across calls)
   std::vector<cudaEvent_t> stage_ev;
   cudaMemPool_t mempool = nullptr;                         // private stream-ordered scratch pool
+  // host-buffer pipeline: persistent device slots (grow-only; inputs at
+  // k * 2 + a, outputs at 8 + k) and their events, kept across calls so the
+  // copies of one call overlap the tail of the previous one
+  std::vector<std::pair<size_t, void *>> pipe_dev;
+  cudaEvent_t pipe_in_ready[4] = {}, pipe_in_free[4] = {}, pipe_out_free[4] = {};
+  bool host_strict = false;  // host inputs read in stream order (lch_set_host_ordering)
+  cudaEvent_t last_h2d = nullptr;  // the pipeline's most recent H2D copy (one of pipe_in_ready)
+  std::vector<cudaEvent_t> trace_ev;  // LCH_PIPE_TRACE: stage events of the host pipeline calls
+  std::vector<size_t> trace_calls;    // first event of each call
   size_t ring_next = 0;
   std::mutex mu;
   std::mutex host_mu;  // serialises the host-buffer entry points (shared staging, pool)
@@ -630,6 +640,14 @@ void lch_destroy(lch_ctx *c) {
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->stage_ev)
       if (e) cudaEventDestroy(e);
+    cudaDeviceSynchronize();
+    for (auto &e : c->pipe_dev)
+      if (e.second) cudaFree(e.second);
+    for (int k = 0; k < 4; ++k) {
+      if (c->pipe_in_ready[k]) cudaEventDestroy(c->pipe_in_ready[k]);
+      if (c->pipe_in_free[k]) cudaEventDestroy(c->pipe_in_free[k]);
+      if (c->pipe_out_free[k]) cudaEventDestroy(c->pipe_out_free[k]);
+    }
     if (c->mempool) {
       cudaDeviceSynchronize();
       cudaMemPoolDestroy(c->mempool);
@@ -897,8 +915,14 @@ static int encode_pow2(lch_ctx *c, const uint16_t *msg, int64_t stride_in, uint1
     for (int i = 0; i < lg_k; ++i) inv.push_back({OP_INV, i, 0u, nullptr});
     if (nb == 2) {
       // rs.py:93-95 with one parity block: fuse inverse and forward(shift k)
-      std::vector<LOp> ops = inv;
-      for (int i = lg_k - 1; i >= 0; --i) ops.push_back({OP_FWD, i, hs_of(c, i, uint32_t(k)), nullptr});
+      // The top inverse level and the first forward level act on the same
+      // pairs: v' = u + v, u' = u + f1 v', then u'' = u' + f2 v', v'' = u'' + v',
+      // i.e. one multiply by f1 + f2 = W^_top(0) + W^_top(k) (the table parts
+      // cancel) -- one op, and every round of the middle pass stays a
+      // straight-line one.
+      std::vector<LOp> ops(inv.begin(), inv.end() - (lg_k > 0 ? 1 : 0));
+      if (lg_k > 0) ops.push_back({OP_INVFWD, lg_k - 1, hs_of(c, lg_k - 1, uint32_t(k)), nullptr});
+      for (int i = lg_k - 2; i >= 0; --i) ops.push_back({OP_FWD, i, hs_of(c, i, uint32_t(k)), nullptr});
       auto plan = plan_passes(ops, lg_k, true, true);
       const int64_t ch = plan.size() > 1 ? chunk_lanes(c, batch, pkt, bs_lane_bytes(R, lg_k)) : batch;
       uint4 *work = nullptr;
@@ -1367,6 +1391,11 @@ struct HostArray {
   // optional host stage: fills rows [r0, r0 + nr) into a page-locked staging
   // buffer (row_bytes per row) that is then copied instead of src
   std::function<void(int64_t r0, int64_t nr, uint8_t *staging)> prep;
+  // with both prep and src set, a chunk goes either through prep (row_bytes
+  // per row) or straight from src (raw_row_bytes per row); `choose` picks per
+  // chunk (true = raw), given whether the H2D stream is idle
+  size_t raw_row_bytes = 0;
+  std::function<bool(int64_t chunk_index, bool h2d_idle)> choose;
 };
 
 // grow-only page-locked staging buffers of the context
@@ -1434,63 +1463,95 @@ int host_streams(lch_ctx *c) {
 
 // ins: host inputs copied per chunk; out: the host output; compute(d_ins,
 // d_out, row0, rows) runs the codec on the caller's stream.
-using ChunkFn = std::function<int(const std::vector<const uint8_t *> &, uint8_t *, int64_t, int64_t)>;
+// raw: the chunk's first input came straight from src (HostArray::choose)
+using ChunkFn = std::function<int(const std::vector<const uint8_t *> &, uint8_t *, int64_t, int64_t, bool raw)>;
+
+// grow-only device buffers of the pipeline slots (kept across calls)
+uint8_t *pipe_buffer(lch_ctx *c, size_t idx, size_t bytes) {
+  std::lock_guard<std::mutex> g(c->mu);
+  if (c->pipe_dev.size() <= idx) c->pipe_dev.resize(idx + 1, {0, nullptr});
+  auto &e = c->pipe_dev[idx];
+  if (e.first < bytes) {
+    if (e.second) {
+      cudaDeviceSynchronize();  // an earlier call may still use the old buffer
+      cudaFree(e.second);
+    }
+    e.second = nullptr;
+    e.first = 0;
+    if (cudaMalloc(&e.second, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    e.first = bytes;
+  }
+  return static_cast<uint8_t *>(e.second);
+}
 
 int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
                   const std::vector<HostArray> &ins, const HostArray &out, const ChunkFn &compute) {
   constexpr int NS = 4;
   LCH_TRY(host_streams(c));
   const int ni = int(ins.size());
-  std::vector<cudaEvent_t> evs;
-  auto mkev = [&](cudaEvent_t &e) -> int {
-    LCH_TRY(cu(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)));
-    evs.push_back(e);
-    return LCH_OK;
-  };
-  struct Guard {
-    std::vector<cudaEvent_t> *v;
-    ~Guard() {
-      for (cudaEvent_t e : *v) cudaEventDestroy(e);
-    }
-  } guard{&evs};
-  Scratch sc(c, s);
+  if (ni > 2) return LCH_EINVAL;
   std::vector<uint8_t *> din(size_t(NS) * ni, nullptr), dout(NS, nullptr);
   for (int k = 0; k < NS; ++k) {
-    for (int a = 0; a < ni; ++a) LCH_TRY(sc.alloc(din[size_t(k) * ni + a], ins[a].row_bytes * size_t(chunk)));
-    LCH_TRY(sc.alloc(dout[k], out.row_bytes * size_t(chunk)));
+    for (int a = 0; a < ni; ++a) {
+      din[size_t(k) * ni + a] =
+          pipe_buffer(c, size_t(k) * 2 + a, std::max(ins[a].row_bytes, ins[a].raw_row_bytes) * size_t(chunk));
+      if (!din[size_t(k) * ni + a]) return LCH_ENOMEM;
+    }
+    dout[k] = pipe_buffer(c, 8 + size_t(k), out.row_bytes * size_t(chunk));
+    if (!dout[k]) return LCH_ENOMEM;
+    for (cudaEvent_t *e : {&c->pipe_in_ready[k], &c->pipe_in_free[k], &c->pipe_out_free[k]})
+      if (!*e) LCH_TRY(cu(cudaEventCreateWithFlags(e, cudaEventDisableTiming)));
   }
-  cudaEvent_t entry, ev_in[NS], ev_done[NS], ev_free[NS];
-  LCH_TRY(mkev(entry));
-  for (int k = 0; k < NS; ++k) {
-    LCH_TRY(mkev(ev_in[k]));
-    LCH_TRY(mkev(ev_done[k]));
-    LCH_TRY(mkev(ev_free[k]));
+  // The slots and their events persist in the context: a slot's input buffer
+  // is refilled once the codec of its previous chunk ran (in_free), its output
+  // buffer once the previous D2H copy ran (out_free) -- in this call or in an
+  // earlier one still in flight.  Host inputs are read right away (they are
+  // complete when the call is made) unless the context asks for stream order.
+  if (c->host_strict) {
+    cudaEvent_t entry = nullptr;
+    LCH_TRY(cu(cudaEventCreateWithFlags(&entry, cudaEventDisableTiming)));
+    cudaError_t e1 = cudaEventRecord(entry, s);
+    cudaError_t e2 = cudaStreamWaitEvent(c->s_h2d, entry, 0);
+    cudaEventDestroy(entry);  // released once the recorded work completes
+    LCH_TRY(cu(e1));
+    LCH_TRY(cu(e2));
   }
-  LCH_TRY(cu(cudaEventRecord(entry, s)));
-  LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, entry, 0)));
-  LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, entry, 0)));
   const int64_t nchunks = (rows + chunk - 1) / chunk;
-  // LCH_PIPE_TRACE=1: per-chunk stage timestamps on stderr (diagnostics)
+  // LCH_PIPE_TRACE=1: per-chunk stage timestamps, printed by
+  // lch_release_host_buffers (diagnostics; no synchronisation in the calls)
   static const bool trace = std::getenv("LCH_PIPE_TRACE") != nullptr;
-  std::vector<cudaEvent_t> tev;
   auto mark = [&](cudaStream_t st) {
     if (!trace) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
-    tev.push_back(e);
+    c->trace_ev.push_back(e);
   };
+  if (trace) c->trace_calls.push_back(c->trace_ev.size());
   mark(s);
   for (int64_t i = 0; i < nchunks; ++i) {
     const int k = int(i % NS);
     const int64_t r0 = i * chunk, nr = std::min(chunk, rows - r0);
-    // input slot k is reusable once the codec of chunk i - NS has consumed it
-    if (i >= NS) LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, ev_done[k], 0)));
+    // input slot k is reusable once the codec of its previous chunk has consumed it
+    LCH_TRY(cu(cudaStreamWaitEvent(c->s_h2d, c->pipe_in_free[k], 0)));
     std::vector<const uint8_t *> dptr(static_cast<size_t>(ni), nullptr);
+    bool raw = false;
     for (int a = 0; a < ni; ++a) {
       const HostArray &h = ins[a];
       uint8_t *d = din[size_t(k) * ni + a];
-      if (h.prep) {
+      if (a == 0 && h.prep && h.src && h.choose) {
+        // the H2D stream is idle when its last recorded copy has completed
+        const bool idle = !c->last_h2d || cudaEventQuery(c->last_h2d) == cudaSuccess;
+        cudaGetLastError();
+        raw = h.choose(i, idle);
+      }
+      if (raw && a == 0) {
+        LCH_TRY(cu(cudaMemcpy2DAsync(d, h.raw_row_bytes, h.src + size_t(r0) * h.pitch, h.pitch, h.raw_row_bytes,
+                                     size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
+      } else if (h.prep) {
         // the staging slot is free once the last H2D copy out of it has run --
         // in this call (chunk i - NS) or in an earlier call still in flight
         const size_t si = size_t(k) * ni + a;
@@ -1514,34 +1575,34 @@ int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
       dptr[size_t(a)] = d;
     }
     mark(c->s_h2d);
-    LCH_TRY(cu(cudaEventRecord(ev_in[k], c->s_h2d)));
-    LCH_TRY(cu(cudaStreamWaitEvent(s, ev_in[k], 0)));
-    // output slot k is reusable once the D2H copy of chunk i - NS has run
-    if (i >= NS) LCH_TRY(cu(cudaStreamWaitEvent(s, ev_free[k], 0)));
-    const int crc = compute(dptr, dout[k], r0, nr);
+    LCH_TRY(cu(cudaEventRecord(c->pipe_in_ready[k], c->s_h2d)));
+    c->last_h2d = c->pipe_in_ready[k];
+    LCH_TRY(cu(cudaStreamWaitEvent(s, c->pipe_in_ready[k], 0)));
+    // output slot k is reusable once the D2H copy of its previous chunk has run
+    LCH_TRY(cu(cudaStreamWaitEvent(s, c->pipe_out_free[k], 0)));
+    const int crc = compute(dptr, dout[k], r0, nr, raw);
     if (crc != LCH_OK) return crc;
     mark(s);
-    LCH_TRY(cu(cudaEventRecord(ev_done[k], s)));
-    LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, ev_done[k], 0)));
+    LCH_TRY(cu(cudaEventRecord(c->pipe_in_free[k], s)));
+    LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, c->pipe_in_free[k], 0)));
     LCH_TRY(cu(cudaMemcpy2DAsync(out.dst + size_t(r0) * out.pitch, out.pitch, dout[k], out.row_bytes,
                                  out.row_bytes, size_t(nr), cudaMemcpyDeviceToHost, c->s_d2h)));
     mark(c->s_d2h);
-    LCH_TRY(cu(cudaEventRecord(ev_free[k], c->s_d2h)));
+    LCH_TRY(cu(cudaEventRecord(c->pipe_out_free[k], c->s_d2h)));
   }
-  if (trace) {
-    cudaDeviceSynchronize();
-    std::fprintf(stderr, "pipeline %lld chunks:", (long long)nchunks);
-    for (size_t i = 1; i < tev.size(); ++i) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, tev[0], tev[i]);
-      std::fprintf(stderr, " %s%.2f", (i - 1) % 3 == 0 ? "| h2d " : (i - 1) % 3 == 1 ? "cmp " : "d2h ", ms);
-    }
-    std::fprintf(stderr, "\n");
-    for (cudaEvent_t e : tev) cudaEventDestroy(e);
-  }
+  // the caller's stream sees the outputs: it waits for the last copies
   for (int64_t i = std::max<int64_t>(0, nchunks - NS); i < nchunks; ++i)
-    LCH_TRY(cu(cudaStreamWaitEvent(s, ev_free[i % NS], 0)));
+    LCH_TRY(cu(cudaStreamWaitEvent(s, c->pipe_out_free[i % NS], 0)));
   return LCH_OK;
+}
+
+// Default rows per chunk: ~64 MiB of the larger per-row transfer, and in row
+// layout whole bit-sliced groups of 1024 codewords (a partial group costs the
+// kernels as much as a full one) once the batch has several.
+int64_t default_chunk(int64_t rows, size_t row_bytes, int64_t pkt) {
+  int64_t chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / std::max<size_t>(row_bytes, 1)));
+  if (!pkt && rows >= 2 * GROUP) chunk = std::max<int64_t>(GROUP, chunk / GROUP * GROUP);
+  return chunk;
 }
 
 int64_t popcount_words(const uint32_t *w, int64_t n) {
@@ -1568,7 +1629,7 @@ int lch_encode_host(lch_ctx *c, const uint16_t *host_msg, int64_t stride_in, uin
   // rows: codewords, or stripe groups of pkt lanes
   const int64_t rows = pkt ? batch / pkt : batch, lanes_per_row = pkt ? pkt : 1;
   const size_t in_row = size_t(k * lanes_per_row) * 2, out_row = size_t((n - k) * lanes_per_row) * 2;
-  if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(32) << 20) / std::max(in_row, out_row)));
+  if (chunk == 0) chunk = default_chunk(rows, std::max(in_row, out_row), pkt);
   chunk = std::min(chunk, rows);
   std::vector<HostArray> ins(1);
   ins[0].src = reinterpret_cast<const uint8_t *>(host_msg);
@@ -1579,7 +1640,7 @@ int lch_encode_host(lch_ctx *c, const uint16_t *host_msg, int64_t stride_in, uin
   out.row_bytes = out_row;
   out.pitch = size_t(stride_out * lanes_per_row) * 2;
   return host_pipeline(c, s, rows, chunk, ins, out,
-                       [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr) {
+                       [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr, bool) {
                          return encode_any(c, reinterpret_cast<const uint16_t *>(d[0]), k,
                                            reinterpret_cast<uint16_t *>(o), n - k, nr * lanes_per_row, k,
                                            pkt, stream);
@@ -1614,13 +1675,21 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
     LCH_TRY(upload_small(c, d_shared, host_bits, size_t(words) * 4, s));
   }
   const size_t in_row = size_t(n * lanes_per_row) * 2, out_row = size_t(k * lanes_per_row) * 2;
-  if (chunk == 0) chunk = std::max<int64_t>(1, int64_t((size_t(64) << 20) / in_row));
+  if (chunk == 0) chunk = default_chunk(rows, in_row / 2, pkt);
   chunk = std::min(chunk, rows);
-  if (shared && !pkt && n >= 32 && !std::getenv("LCH_NO_COMPACT")) {
-    // Only the survivors cross PCIe: the host compacts each row (AVX-512
-    // compress-store on the worker pool) into page-locked staging, the
-    // device expands the rows back (erased positions read as zero; the
-    // decoder ignores them, rs.py:130-134).
+  // LCH_COMPACT = all | none | alt | auto (default): which chunks of a
+  // shared-pattern decode are compacted on the host (below)
+  const char *cmode_env = std::getenv("LCH_COMPACT");
+  const std::string cmode = std::getenv("LCH_NO_COMPACT") ? "none" : (cmode_env ? cmode_env : "auto");
+  if (shared && !pkt && n >= 32 && cmode != "none") {
+    // Only the survivors need to cross PCIe: the host compacts each row
+    // (AVX-512 compress-store on the worker pool) into page-locked staging,
+    // the device expands the rows back (erased positions read as zero; the
+    // decoder ignores them, rs.py:130-134).  Compaction trades PCIe bytes for
+    // host memory traffic (it reads the row and writes the survivors before
+    // the DMA reads them again), so it is decided per chunk: a chunk is
+    // compacted while the H2D stream still has copies to run (the host work
+    // then hides behind them) and sent as it is when the stream has run dry.
     const int64_t surv = n - counts[0];
     std::vector<int32_t> rank(static_cast<size_t>(n), -1);
     for (int64_t j = 0, r = 0; j < n; ++j)
@@ -1630,19 +1699,27 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
     LCH_TRY(upload_small(c, d_rank, rank.data(), size_t(n) * 4, s));
     HostPool &pool = host_pool(c);
     const size_t crow = size_t(std::max<int64_t>(surv, 1)) * 2;
-    if (chunk == 0 || chunk > rows) chunk = std::min(rows, std::max<int64_t>(1, int64_t((size_t(64) << 20) / (size_t(n) * 2))));
     std::vector<HostArray> cins(1);
     cins[0].row_bytes = crow;
     cins[0].prep = [&](int64_t r0, int64_t nr, uint8_t *stg) {
       compact_rows(pool, host_rx + r0 * stride_in, stride_in, host_bits, n, nr,
                    reinterpret_cast<uint16_t *>(stg), std::max<int64_t>(surv, 1));
     };
+    if (cmode != "all") {
+      cins[0].src = reinterpret_cast<const uint8_t *>(host_rx);
+      cins[0].pitch = size_t(stride_in) * 2;
+      cins[0].raw_row_bytes = size_t(n) * 2;
+      cins[0].choose = [&](int64_t ci, bool idle) { return cmode == "alt" ? (ci & 1) != 0 : idle; };
+    }
     HostArray cout;
     cout.dst = reinterpret_cast<uint8_t *>(host_out);
     cout.row_bytes = size_t(k) * 2;
     cout.pitch = size_t(stride_out) * 2;
     return host_pipeline(c, s, rows, chunk, cins, cout,
-                         [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr) {
+                         [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t, int64_t nr, bool raw) {
+                           if (raw)  // the chunk arrived as it is: rows of n symbols
+                             return decode_any(c, reinterpret_cast<const uint16_t *>(d[0]), n, d_shared, 1,
+                                               reinterpret_cast<uint16_t *>(o), k, nr, k, 0, counts.data(), stream);
                            Scratch cs(c, s);
                            uint16_t *full = nullptr;
                            LCH_TRY(cs.alloc(full, size_t(nr) * size_t(n)));
@@ -1657,7 +1734,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
   for (int64_t v : counts) min_erased = std::min(min_erased, v);
   // packing pays only when a large share of the packets is erased (the host
   // copy of the survivors then costs less than moving the erased ones)
-  if (pkt && 5 * min_erased >= 2 * n && !std::getenv("LCH_NO_COMPACT")) {
+  if (pkt && 5 * min_erased >= 2 * n && cmode != "none") {
     // Packet layout (stripe groups): erasures are whole packets, so only the
     // surviving packets cross PCIe -- the host packs them (memcpy per packet
     // on the worker pool) into page-locked staging, the device scatters them
@@ -1698,7 +1775,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
     cout.row_bytes = size_t(k) * pkt_bytes;
     cout.pitch = size_t(stride_out) * pkt_bytes;
     return host_pipeline(c, s, rows, chunk, cins, cout,
-                         [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr) {
+                         [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr, bool) {
                            Scratch cs(c, s);
                            const int64_t npat = shared ? 1 : nr;
                            std::vector<int32_t> rank(size_t(npat) * size_t(n), -1);
@@ -1737,7 +1814,7 @@ int lch_decode_host(lch_ctx *c, const uint16_t *host_rx, int64_t stride_in, cons
   out.row_bytes = out_row;
   out.pitch = size_t(stride_out * lanes_per_row) * 2;
   return host_pipeline(c, s, rows, chunk, ins, out,
-                       [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr) {
+                       [&](const std::vector<const uint8_t *> &d, uint8_t *o, int64_t r0, int64_t nr, bool) {
                          const uint32_t *bits = shared ? d_shared : reinterpret_cast<const uint32_t *>(d[1]);
                          return decode_any(c, reinterpret_cast<const uint16_t *>(d[0]), n, bits, shared,
                                            reinterpret_cast<uint16_t *>(o), k, nr * lanes_per_row, k, pkt,
@@ -1749,6 +1826,46 @@ int lch_compact_rows(lch_ctx *c, const uint16_t *host_rx, int64_t stride, const 
                      int64_t n, int64_t rows, uint16_t *host_out, int64_t out_stride) {
   if (!c || !host_rx || !host_bits || !host_out || n < 0 || rows < 0 || stride < n) return LCH_EINVAL;
   compact_rows(host_pool(c), host_rx, stride, host_bits, n, rows, host_out, out_stride);
+  return LCH_OK;
+}
+
+int lch_set_host_ordering(lch_ctx *c, int stream_ordered) {
+  if (!c) return LCH_EINVAL;
+  std::lock_guard<std::mutex> hg(c->host_mu);
+  c->host_strict = stream_ordered != 0;
+  return LCH_OK;
+}
+
+int lch_release_host_buffers(lch_ctx *c) {
+  if (!c) return LCH_EINVAL;
+  std::lock_guard<std::mutex> hg(c->host_mu);
+  if (!c->dev_ready) return LCH_OK;
+  LCH_TRY(ensure_device(c));
+  LCH_TRY(cu(cudaDeviceSynchronize()));
+  std::lock_guard<std::mutex> g(c->mu);
+  if (!c->trace_ev.empty()) {  // LCH_PIPE_TRACE: ms since the first call's entry
+    for (size_t ci = 0; ci < c->trace_calls.size(); ++ci) {
+      const size_t b = c->trace_calls[ci], e = ci + 1 < c->trace_calls.size() ? c->trace_calls[ci + 1] : c->trace_ev.size();
+      std::fprintf(stderr, "call %zu:", ci);
+      for (size_t i = b + 1; i < e; ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->trace_ev[0], c->trace_ev[i]);
+        std::fprintf(stderr, " %s%.2f", (i - b - 1) % 3 == 0 ? "| h2d " : (i - b - 1) % 3 == 1 ? "cmp " : "d2h ", ms);
+      }
+      std::fprintf(stderr, "\n");
+    }
+    for (cudaEvent_t e : c->trace_ev) cudaEventDestroy(e);
+    c->trace_ev.clear();
+    c->trace_calls.clear();
+  }
+  for (auto &e : c->pipe_dev) {
+    if (e.second) cudaFree(e.second);
+    e = {0, nullptr};
+  }
+  for (auto &e : c->pinned) {
+    if (e.second) cudaFreeHost(e.second);
+    e = {0, nullptr};
+  }
   return LCH_OK;
 }
 

@@ -742,27 +742,27 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
 // half): forward transform.py:126-133 (u' = u + f v, v' = u' + v) or inverse
 // transform.py:165-169 (v' = u + v, u' = u + f v').  f is warp-uniform.
 template <int R, uint32_t POLY>
-__device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, bool inv,
+__device__ __forceinline__ void butterfly(uint32_t (&u)[R], uint32_t (&v)[R], uint32_t f, int kind,
                                           const Mul<R, POLY> &mm) {
   using F = GF<R, 16u>;  // xor_into only (polynomial-independent)
-  if (inv) F::xor_into(v, u);
+  if (kind != OP_FWD) F::xor_into(v, u);
   // zero factors (block 0 of every level at shift 0, transform.py:154-161)
   // are a warp-uniform skip
   if (f) mm.acc(u, v, f);
-  if (!inv) F::xor_into(v, u);
+  if (kind != OP_INV) F::xor_into(v, u);
 }
 
 // Two butterflies sharing one factor (pairs (u0, v0) and (u1, v1)).
 template <int R, uint32_t POLY>
 __device__ __forceinline__ void butterfly2(uint32_t (&u0)[R], uint32_t (&v0)[R], uint32_t (&u1)[R],
-                                           uint32_t (&v1)[R], uint32_t f, bool inv, const Mul<R, POLY> &mm) {
+                                           uint32_t (&v1)[R], uint32_t f, int kind, const Mul<R, POLY> &mm) {
   using F = GF<R, 16u>;
-  if (inv) {
+  if (kind != OP_FWD) {
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);
   }
   if (f) mm.acc2(u0, v0, u1, v1, f);
-  if (!inv) {
+  if (kind != OP_INV) {
     F::xor_into(v0, u0);
     F::xor_into(v1, u1);
   }
@@ -789,7 +789,9 @@ struct FactorLoader {
         const int m = op.mloc;
         const int qu = ((pp >> m) << (m + 1)) | (pp & ((1 << m) - 1));
         const int lvl = op.level;
-        v[k] = uint32_t(__ldg(p.w_hat + p.w_hat_off[lvl] + ((base | tpos[qu]) >> (lvl + 1)))) ^ op.hs;
+        v[k] = op.kind == OP_INVFWD
+                   ? op.hs
+                   : uint32_t(__ldg(p.w_hat + p.w_hat_off[lvl] + ((base | tpos[qu]) >> (lvl + 1)))) ^ op.hs;
         if (PDBG(256)) v[k] = uint32_t(p.dbg) >> 16;  // experiment: one forced factor
         slot[k] = o * (1 << TPB_MAX) + qu;
       }
@@ -953,9 +955,33 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
         // straight-line rounds: [op along m0] or [op along m0, op along m1];
         // ops whose pairs share the factor run as one two-vector multiply
         const uint32_t *ft = fac[fb] + rr.op_begin * (1 << TPB_MAX);
+        if constexpr (PAT == 3) {
+          // pattern 3 (launch_pass rewrites the rounds): a round is the op with
+          // distinct factors along m0 (shape 1, 2) and/or the op with a shared
+          // factor along m1 (shape 2, 3), in either order (rev: m1 first), so
+          // one copy of each multiply body serves inverse, forward and mixed
+          // passes
+          const bool has_d = rr.shape != 3, has_s = rr.shape != 1;
+          const int kd = p.ops[rr.op_begin].kind, ks = p.ops[rr.op_begin + (has_d ? 1 : 0)].kind;
+          const uint32_t *fs = ft + (has_d ? (1 << TPB_MAX) : 0);
+#pragma unroll 1
+          for (int step = 0; step < 2; ++step) {
+            if ((step == 0) == (rr.rev != 0)) {
+              if (has_s) {
+                const uint32_t f = __shfl_sync(0xffffffffu, fs[q0], 0);
+                butterfly2<R, POLY>(a0, a2, a1, a3, f, ks, mm);
+              }
+            } else if (has_d) {
+              const uint32_t f1 = __shfl_sync(0xffffffffu, ft[q0], 0);
+              const uint32_t f2 = __shfl_sync(0xffffffffu, ft[q0 | M1], 0);
+              butterfly<R, POLY>(a0, a1, f1, kd, mm);
+              butterfly<R, POLY>(a2, a3, f2, kd, mm);
+            }
+          }
+        } else {
         const PassOp &oa = p.ops[rr.op_begin];
         const uint32_t fa = __shfl_sync(0xffffffffu, ft[q0], 0);
-        const bool inv_a = PAT == 2 ? false : oa.kind == OP_INV;
+        const int inv_a = PAT == 2 ? int(OP_FWD) : oa.kind;
         if (PAT ? PAT == 2 : oa.shared) {
           butterfly2<R, POLY>(a0, a1, a2, a3, fa, inv_a, mm);
         } else {
@@ -967,7 +993,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
           const uint32_t *fu = ft + (1 << TPB_MAX);
           const PassOp &ob = p.ops[rr.op_begin + 1];
           const uint32_t fb1 = __shfl_sync(0xffffffffu, fu[q0], 0);
-          const bool inv_b = PAT == 2 ? false : ob.kind == OP_INV;
+          const int inv_b = PAT == 2 ? int(OP_FWD) : ob.kind;
           if (PAT ? PAT == 1 : ob.shared) {
             butterfly2<R, POLY>(a0, a2, a1, a3, fb1, inv_b, mm);
           } else {
@@ -975,6 +1001,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
             butterfly<R, POLY>(a0, a2, fb1, inv_b, mm);
             butterfly<R, POLY>(a1, a3, fb2, inv_b, mm);
           }
+        }
         }
         if (!last_reg && !(PDBG(32))) {
           Blk<R>::store(blk(q0), lane, a0);
@@ -989,7 +1016,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
         bool sw = false;
         for (int o = rr.op_begin; o < ((PDBG(2)) ? rr.op_begin : rr.op_end); ++o) {
           const PassOp &op = p.ops[o];
-          const bool inv = op.kind == OP_INV;
+          const int inv = op.kind;
           if (op.m == 1 && !sw) {
 #pragma unroll
             for (int b = 0; b < R; ++b) {
@@ -1194,6 +1221,7 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 13>(const PassParams &, 
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 42>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 56>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1647,6 +1675,45 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       if (ok && (vp == 24 || vp == 25 || vp == 28 || vp == 29 || vp == 40 || vp == 42 || vp == 44 || vp == 46)) {
         v = vp;
         break;
+      }
+    }
+  }
+  // mixed inverse / forward rounds (the encode's fused middle pass): the
+  // pattern-3 instance runs every straight-line round from one copy of each
+  // multiply body.  Its rounds are [distinct-factor op along m0] and/or
+  // [shared-factor op along m1] in either order, so forward rounds swap their
+  // bits (of a round's two levels the higher one always shares its factor).
+  PassParams p3;
+  static const bool force3 = std::getenv("LCH_FORCE_PAT3") != nullptr;
+  if constexpr (R == 16 && POLY != 0u) {
+    if (shaped && (v == 8 || (force3 && (v == 24 || v == 40)))) {
+      p3 = p;
+      bool ok = true;
+      for (int r = 0; r < p3.nrounds && ok; ++r) {
+        PassRound &rr = p3.rounds[r];
+        PassOp &a = p3.ops[rr.op_begin];
+        rr.rev = 0;
+        if (rr.shape == 2) {
+          PassOp &b = p3.ops[rr.op_begin + 1];
+          if (a.shared && !b.shared) {
+            std::swap(a, b);
+            std::swap(rr.m0, rr.m1);
+            a.m = 0;
+            b.m = 1;
+            rr.rev = 1;
+          } else if (a.shared || !b.shared) {
+            ok = false;
+          }
+        } else if (a.shared) {  // a single shared-factor op: along m1
+          std::swap(rr.m0, rr.m1);
+          a.m = 1;
+          rr.shape = 3;
+        }
+      }
+      if (ok) {
+        const size_t smem3 = pass_smem_bytes(R, p.tpb, false);
+        const int64_t total3 = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
+        return launch_pass_v<R, POLY, 56>(p3, unsigned(std::min<int64_t>(total3, int64_t(4) * sm_count())), smem3, s);
       }
     }
   }

@@ -16,7 +16,10 @@ constexpr int MAXOPS = 24;
 constexpr int MAXROUNDS = 12;
 constexpr int MAXSCALE = 4;
 
-enum OpKind : int { OP_FWD = 0, OP_INV = 1, OP_SCALE = 2 };
+// OP_INVFWD: an inverse level followed by the forward level on the same bit,
+// v' = u + v; u'' = u + (f_inv + f_fwd) v'; v'' = u'' + v' (one multiply; the
+// table parts of the two factors cancel, so its factor is hs alone)
+enum OpKind : int { OP_FWD = 0, OP_INV = 1, OP_SCALE = 2, OP_INVFWD = 3 };
 enum IoMode : int { IO_BS = 0, IO_RAW = 1 };
 
 struct PassOp {
@@ -40,7 +43,9 @@ struct PassRound {
   int obit[TPB_MAX];
   int op_begin, op_end;   // butterfly ops of the round in ops[]
   uint8_t q0w[NWARP];     // warp w's first tile position (obit[] spread of w), precomputed
-  int shape;              // 0 general; 1: one op along m0; 2: one along m0 then one along m1
+  int shape;              // 0 general; 1: one op along m0; 2: one along m0 then one along m1;
+                          // 3 (pattern-3 instances): one op along m1
+  int rev;                // pattern-3 instances: the op along m1 runs first
 };
 
 // Raw uint16 batch: element (b, j) at ptr[b * row_stride + j].

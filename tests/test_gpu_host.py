@@ -191,3 +191,106 @@ def test_back_to_back_decode_host_calls_keep_their_staging(lch, bt16):
     torch.cuda.synchronize()
     for out, msg in zip(outs, msgs):
         np.testing.assert_array_equal(out.numpy().view(np.uint16), msg)
+
+
+def test_interleaved_host_calls_overlap_across_calls(lch, bt16):
+    """encode_host / decode_host queued alternately on different buffers with a
+    single host sync at the end: the persistent pipeline slots let the copies
+    of one call overlap the tail of the previous one, and every call must
+    still produce its own result (slot reuse is ordered by the context's
+    per-slot events across calls)."""
+    import torch
+    from paper_1404_3458_b200._lib import bitmask_from_positions
+    from paper_1404_3458_b200.rs import decode_host, encode_host
+    n, k, B = 1 << 16, 1 << 15, 2100
+    cp = lch.CodeParams(16, k)
+    mask = O.gen_erasures(22, n, n - k, 0, 1)[0].astype(bool)
+    bits = bitmask_from_positions(n, np.nonzero(mask)[0])
+    msgs = [O.gen_symbols(seed, 16, 0, B, k) for seed in (51, 52, 53)]
+    hmsgs = [pinned(m) for m in msgs]
+    refs = []
+    for hm in hmsgs:  # reference parity, one call at a time
+        hp = torch.empty((B, n - k), dtype=torch.int16, pin_memory=True)
+        encode_host(cp, bt16, hm, hp)
+        torch.cuda.synchronize()
+        refs.append(hp.numpy().view(np.uint16).copy())
+    rxs = []
+    for m, p in zip(msgs, refs):
+        rx = np.concatenate([m, p], axis=1)
+        rx[:, mask] = 0xABCD
+        rxs.append(pinned(rx))
+    pars = [torch.empty((B, n - k), dtype=torch.int16, pin_memory=True) for _ in msgs]
+    outs = [torch.empty((B, k), dtype=torch.int16, pin_memory=True) for _ in msgs]
+    for chunk in (0, 300):
+        for t in pars + outs:
+            t.zero_()
+        for hm, hp, hrx, out in zip(hmsgs, pars, rxs, outs):
+            encode_host(cp, bt16, hm, hp, chunk)
+            decode_host(cp, bt16, hrx, bits, out, chunk)
+        torch.cuda.synchronize()
+        for m, p, hp, out in zip(msgs, refs, pars, outs):
+            np.testing.assert_array_equal(hp.numpy().view(np.uint16), p)
+            np.testing.assert_array_equal(out.numpy().view(np.uint16), m)
+    # one sampled row against the oracle
+    orc = O.Oracle(16)
+    np.testing.assert_array_equal(refs[1][7], orc.encode(k, msgs[1][7])[k:])
+
+
+def test_stream_ordered_host_inputs(lch, bt16):
+    """lch_set_host_ordering(ctx, 1): a call may read a host buffer that an
+    earlier call on the same stream is still writing (parity of the parity,
+    chained without a host sync); released buffers are re-created on demand."""
+    import torch
+    from paper_1404_3458_b200 import _lib
+    from paper_1404_3458_b200.rs import encode_device, encode_host
+    n, k, B = 1 << 16, 1 << 15, 1500
+    cp = lch.CodeParams(16, k)
+    msg = O.gen_symbols(61, 16, 0, B, k)
+    hm = pinned(msg)
+    p1 = torch.zeros((B, k), dtype=torch.int16, pin_memory=True)
+    p2 = torch.zeros((B, k), dtype=torch.int16, pin_memory=True)
+    h = bt16.ctx.handle
+    _lib.check(_lib.lib.lch_release_host_buffers(h))
+    _lib.check(_lib.lib.lch_set_host_ordering(h, 1))
+    try:
+        encode_host(cp, bt16, hm, p1, 256)
+        encode_host(cp, bt16, p1, p2, 256)
+        torch.cuda.synchronize()
+    finally:
+        _lib.check(_lib.lib.lch_set_host_ordering(h, 0))
+    d1 = torch.empty((B, k), dtype=torch.int16, device="cuda")
+    d2 = torch.empty((B, k), dtype=torch.int16, device="cuda")
+    encode_device(cp, bt16, hm.cuda(), d1)
+    encode_device(cp, bt16, d1, d2)
+    torch.cuda.synchronize()
+    assert torch.equal(p1, d1.cpu())
+    assert torch.equal(p2, d2.cpu())
+
+
+@pytest.mark.parametrize("mode", ["all", "alt", "none", "auto"])
+def test_decode_host_compaction_modes(lch, bt16, mode, monkeypatch):
+    """Shared-pattern decode_host with the survivors compacted on the host for
+    all / every other / no / automatically chosen chunks (LCH_COMPACT): the
+    same output in every mode, non-codeword rows included."""
+    import torch
+    from paper_1404_3458_b200._lib import bitmask_from_positions
+    from paper_1404_3458_b200.rs import decode_host
+    n, k, B = 1 << 16, 1 << 15, 700
+    cp = lch.CodeParams(16, k)
+    mask = O.gen_erasures(71, n, n - k, 0, 1)[0].astype(bool)
+    bits = bitmask_from_positions(n, np.nonzero(mask)[0])
+    rx = O.gen_symbols(72, 16, 0, B, n)  # arbitrary received words (not codewords)
+    hrx = pinned(rx)
+    monkeypatch.setenv("LCH_COMPACT", mode)
+    out = torch.zeros((B, k), dtype=torch.int16, pin_memory=True)
+    decode_host(cp, bt16, hrx, bits, out, 96)
+    torch.cuda.synchronize()
+    got = out.numpy().view(np.uint16)
+    orc = O.Oracle(16)
+    for r in (0, 95, 96, 191, B - 1):
+        np.testing.assert_array_equal(got[r], orc.decode(k, rx[r], mask.astype(np.uint8)))
+    monkeypatch.setenv("LCH_COMPACT", "all")
+    ref = torch.zeros((B, k), dtype=torch.int16, pin_memory=True)
+    decode_host(cp, bt16, hrx, bits, ref, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)

@@ -36,7 +36,8 @@ for name, fn in [("encode_host", lambda: encode_host(cp, bt, h_msg, h_par)),
                  ("both", lambda: (encode_host(cp, bt, h_msg, h_par), decode_host(cp, bt, h_rx, bits, h_out)))]:
     ev, wall = timeit(fn)
     print(f"{name}: {ev:.2f} ms (events), {wall:.2f} ms wall")
-os.environ["LCH_NO_COMPACT"] = "1"
-ev, wall = timeit(lambda: decode_host(cp, bt, h_rx, bits, h_out))
-print(f"decode_host no-compact: {ev:.2f} ms (events), {wall:.2f} ms wall")
-t0 = time.perf_counter(); h_rx.numpy().view(np.uint16)[:, ::2].copy(); print("numpy strided copy ms", (time.perf_counter()-t0)*1e3)
+for mode in ("all", "none", "alt", "auto", "all", "none", "auto"):
+    os.environ["LCH_COMPACT"] = mode
+    ev, _ = timeit(lambda: decode_host(cp, bt, h_rx, bits, h_out), 6)
+    ev2, _ = timeit(lambda: (encode_host(cp, bt, h_msg, h_par), decode_host(cp, bt, h_rx, bits, h_out)), 6)
+    print(f"LCH_COMPACT={mode}: decode_host {ev:.2f} ms, both {ev2:.2f} ms")

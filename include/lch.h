@@ -189,6 +189,10 @@ int lch_decode_host(lch_ctx *ctx, const uint16_t *host_rx, int64_t stride_in,
  * stream order (after the work already queued on `stream`); 0 (default): at
  * the call. */
 int lch_set_host_ordering(lch_ctx *ctx, int stream_ordered);
+/* Bytes the host-buffer entry points have queued for host->device and
+ * device->host copies since the context was created (bench accounting: a
+ * shared-pattern decode sends a chunk compacted or as it is). */
+int lch_host_copy_bytes(lch_ctx *ctx, uint64_t *h2d_bytes, uint64_t *d2h_bytes);
 /* Waits for the device and frees the pipeline's persistent device slots and
  * page-locked staging buffers (they are re-created on demand). */
 int lch_release_host_buffers(lch_ctx *ctx);

@@ -58,6 +58,7 @@ def _load() -> ctypes.CDLL:
         "lch_set_scratch_limit": ([P, u64], i32),
         "lch_set_host_ordering": ([P, i32], i32),
         "lch_release_host_buffers": ([P], i32),
+        "lch_host_copy_bytes": ([P, P, P], i32),
         "lch_compact_rows": ([P, P, i64, P, i64, i64, P, i64], i32),
         "lch_encode_host": ([P, P, i64, P, i64, i64, i64, i64, i64, P], i32),
         "lch_decode_host": ([P, P, i64, P, i32, P, i64, i64, i64, i64, i64, P], i32),

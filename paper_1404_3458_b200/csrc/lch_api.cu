@@ -50,6 +50,7 @@ struct lch_ctx {
   cudaEvent_t pipe_in_ready[4] = {}, pipe_in_free[4] = {}, pipe_out_free[4] = {};
   bool host_strict = false;  // host inputs read in stream order (lch_set_host_ordering)
   cudaEvent_t last_h2d = nullptr;  // the pipeline's most recent H2D copy (one of pipe_in_ready)
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;  // bytes the host pipeline queued (lch_host_copy_bytes)
   std::vector<cudaEvent_t> trace_ev;  // LCH_PIPE_TRACE: stage events of the host pipeline calls
   std::vector<size_t> trace_calls;    // first event of each call
   size_t ring_next = 0;
@@ -1548,6 +1549,7 @@ int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
         cudaGetLastError();
         raw = h.choose(i, idle);
       }
+      c->h2d_bytes += uint64_t(raw && a == 0 ? h.raw_row_bytes : h.row_bytes) * uint64_t(nr);
       if (raw && a == 0) {
         LCH_TRY(cu(cudaMemcpy2DAsync(d, h.raw_row_bytes, h.src + size_t(r0) * h.pitch, h.pitch, h.raw_row_bytes,
                                      size_t(nr), cudaMemcpyHostToDevice, c->s_h2d)));
@@ -1587,6 +1589,7 @@ int host_pipeline(lch_ctx *c, cudaStream_t s, int64_t rows, int64_t chunk,
     LCH_TRY(cu(cudaStreamWaitEvent(c->s_d2h, c->pipe_in_free[k], 0)));
     LCH_TRY(cu(cudaMemcpy2DAsync(out.dst + size_t(r0) * out.pitch, out.pitch, dout[k], out.row_bytes,
                                  out.row_bytes, size_t(nr), cudaMemcpyDeviceToHost, c->s_d2h)));
+    c->d2h_bytes += uint64_t(out.row_bytes) * uint64_t(nr);
     mark(c->s_d2h);
     LCH_TRY(cu(cudaEventRecord(c->pipe_out_free[k], c->s_d2h)));
   }
@@ -1833,6 +1836,14 @@ int lch_set_host_ordering(lch_ctx *c, int stream_ordered) {
   if (!c) return LCH_EINVAL;
   std::lock_guard<std::mutex> hg(c->host_mu);
   c->host_strict = stream_ordered != 0;
+  return LCH_OK;
+}
+
+int lch_host_copy_bytes(lch_ctx *c, uint64_t *h2d, uint64_t *d2h) {
+  if (!c) return LCH_EINVAL;
+  std::lock_guard<std::mutex> hg(c->host_mu);
+  if (h2d) *h2d = c->h2d_bytes;
+  if (d2h) *d2h = c->d2h_bytes;
   return LCH_OK;
 }
 

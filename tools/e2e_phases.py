@@ -36,7 +36,7 @@ for name, fn in [("encode_host", lambda: encode_host(cp, bt, h_msg, h_par)),
                  ("both", lambda: (encode_host(cp, bt, h_msg, h_par), decode_host(cp, bt, h_rx, bits, h_out)))]:
     ev, wall = timeit(fn)
     print(f"{name}: {ev:.2f} ms (events), {wall:.2f} ms wall")
-for mode in ("all", "none", "alt", "auto", "all", "none", "auto"):
+for mode in ("all", "auto", "all", "auto"):
     os.environ["LCH_COMPACT"] = mode
     ev, _ = timeit(lambda: decode_host(cp, bt, h_rx, bits, h_out), 6)
     ev2, _ = timeit(lambda: (encode_host(cp, bt, h_msg, h_par), decode_host(cp, bt, h_rx, bits, h_out)), 6)

@@ -104,7 +104,12 @@ def full(path, out, traffic_out=None):
                for d in launches_]
         dram = [num(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 0))
                 for d in launches_]
+        dur = [num(d["gpu__time_duration.sum"]) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1,
+                                                     "msecond": 1e3, "ms": 1e3}.get(u["gpu__time_duration.sum"], 1)
+               for d in launches_]
         json.dump({"source": path, "kernel": launches_[0].get("Kernel Name", "")[:80],
+                   "kernels": [d.get("Kernel Name", "")[:60] for d in launches_],
+                   "duration_us_per_launch": [round(x, 3) for x in dur],
                    "dram_bytes_per_launch": int(sum(tb) / len(tb)),
                    "per_launch": [int(x) for x in tb],
                    "alu_pipe_pct_per_launch": alu, "dram_pct_per_launch": dram},

@@ -659,6 +659,60 @@ __device__ __forceinline__ void store_tile_raw(const PassParams &p, uint4 *smem,
   }
 }
 
+// Raw row-major output straight from the last round's registers (R = 16, row
+// layout, tile = positions 32t .. 32t+31 inside the output window, last round
+// over tile bits 1 and 0): the thread's four blocks are the consecutive
+// positions q0 .. q0+3 (x0..x3) of its lane-word, so two 32x32 bit transposes
+// in registers give, for every L, the 8 bytes of row 32L + lane at those
+// positions.  The rows leave through a half-tile staging area in the spare
+// shared memory (512 rows x 64 B at a time, the column-major swizzled word
+// layout of stage_idx) as coalesced 16-byte row chunks -- while the next
+// tile's blocks already stream into the tile buffer.
+__device__ __forceinline__ int stage_idx_h(int r, int cw) { return cw * (GROUP / 2) + (r ^ (8 * ((cw >> 2) & 3))); }
+
+__device__ __forceinline__ void store_rows_from_regs(const PassParams &p, uint4 *smem, int g, uint32_t base,
+                                                     int q0, uint32_t (&x0)[16], uint32_t (&x1)[16],
+                                                     uint32_t (&x2)[16], uint32_t (&x3)[16]) {
+  uint32_t *rs = reinterpret_cast<uint32_t *>(smem + stage_offset_u4<16>());
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t A[32], B[32];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    A[k] = x0[k];
+    A[16 + k] = x1[k];
+    B[k] = x2[k];
+    B[16 + k] = x3[k];
+  }
+  transpose32(A);
+  transpose32(B);
+  const int cw = q0 >> 1;
+  const RawIO &io = p.raw_out;
+  const int64_t row0 = int64_t(g) * GROUP;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      rs[stage_idx_h(32 * l + lane, cw)] = A[16 * h + l];
+      rs[stage_idx_h(32 * l + lane, cw + 1)] = B[16 * h + l];
+    }
+    __syncthreads();
+    if (!(PDBG(5))) {
+#pragma unroll 4
+      for (int i = 0; i < (GROUP / 2) * 4 / NT; ++i) {
+        const int idx = tid + i * NT;
+        const int r = idx >> 2, c = idx & 3;
+        const int64_t b = row0 + (GROUP / 2) * h + r;
+        if (b < p.batch) {
+          const uint4 val = make_uint4(rs[stage_idx_h(r, 4 * c + 0)], rs[stage_idx_h(r, 4 * c + 1)],
+                                       rs[stage_idx_h(r, 4 * c + 2)], rs[stage_idx_h(r, 4 * c + 3)]);
+          reinterpret_cast<uint4 *>(const_cast<uint16_t *>(raw_addr(io, b, base)))[c] = val;
+        }
+      }
+    }
+    if (h == 0) __syncthreads();  // half 1 refills the staging area
+  }
+}
+
 }  // namespace
 
 // Multiplier: the compile-time-polynomial GF<R, POLY>, or (POLY == 0) the
@@ -824,6 +878,9 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
   // distinct factors, op along m1 shared), 2: forward (m0 shared, m1 distinct)
   constexpr int PAT = (V >> 4) & 3;
   constexpr bool ROWONLY = V & 128;  // raw I/O in row layout only (no packet paths)
+  // bit 9: raw row-major output straight from the last round's registers
+  // (launch_pass picks it when every tile qualifies, see store_rows_from_regs)
+  constexpr bool RREG = (V & 512) && R == 16;
   constexpr int U4 = Blk<R>::U4;
   // 128-byte aligned: TMA tensor copies land here
   extern __shared__ __align__(128) uint4 smem[];
@@ -893,7 +950,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
   // BS output, so the next tile's loads can stream into shared memory while
   // it computes.
   const bool reg_path = p.nrounds > 0 && (!POST_OK || (p.npost == 0 && !p.gt_out)) &&
-                        (!ROUT || p.out_mode == IO_BS);
+                        (!ROUT || p.out_mode == IO_BS || RREG);
 
   for (;;) {
     const int next = tl + int(gridDim.x);
@@ -1056,6 +1113,11 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
         // streaming stores per chunk (no staging, no wait on earlier stores),
         // overlapping the next tile's rounds.
         uint4 *dst = p.bs_out + ((size_t(g) << p.lgH) * U4);
+        if constexpr (RREG) {
+          // forward pattern, last round over bits (1, 0): a0, a2, a1, a3 are
+          // the positions q0, q0 + 1, q0 + 2, q0 + 3
+          store_rows_from_regs(p, smem, g, base, q0, a0, a2, a1, a3);
+        } else
         if (active && !(PDBG(5))) {
           Blk<R>::store_g(dst + size_t(base | tpos[q0]) * U4, lane, a0);
           Blk<R>::store_g(dst + size_t(base | tpos[q0 | M0]) * U4, lane, a1);
@@ -1222,6 +1284,7 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 44>(const PassParams &, 
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 42>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 56>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 682>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1724,6 +1787,18 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
     const int vs = v | (!(p.npost || p.gt_out) ? 64 : !p.npre ? 256 : 0);
     if (vs == 221 || vs == 108 || vs == 284 || vs == 430) v = vs;
   }
+  // raw output from the last round's registers: every tile inside the output
+  // window, row layout, 16-byte aligned rows, no merge, last round over tile
+  // bits (1, 0) in the forward pattern
+  static const bool no_rreg = std::getenv("LCH_NO_RREG") != nullptr;
+  if (R == 16 && v == 170 && !no_rreg && p.tpb == 5 && p.nrounds > 0) {
+    const RawIO &o = p.raw_out;
+    const PassRound &lr = p.rounds[p.nrounds - 1];
+    bool ok = o.pkt == 0 && o.vec && !o.merge_src && o.pos_lo == 0 && o.pos_hi >= (int64_t(1) << p.lgH) &&
+              lr.shape == 2 && lr.m0 == 1 && lr.m1 == 0 && p.npost == 0 && !p.gt_out;
+    for (int m = 0; m < p.tpb; ++m) ok = ok && p.gbit[m] == m;
+    if (ok) v = 682;
+  }
   if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, p.out_mode == IO_RAW);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
@@ -1759,6 +1834,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 44: return launch_pass_v<R, POLY, 44>(p, ctas, smem, s);
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);
       case 42: return launch_pass_v<R, POLY, 42>(p, ctas, smem, s);
+      case 682: return launch_pass_v<R, POLY, 682>(p, ctas, smem, s);
       default: return launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
     }
   } else {  // r = 8: the lean and the generic instance only

@@ -366,6 +366,37 @@ __device__ __forceinline__ void finish_tile_raw_tma(uint4 *smem) {
   Blk<R>::store(bs + 3 * Blk<R>::U4, lane, x);
 }
 
+// The same conversion straight into the registers of a first round over tile
+// bits (0, 1): after the transposes warp w holds the four consecutive
+// positions 4w .. 4w+3 of its lane-word -- exactly that round's operands, so
+// the tile skips one shared-memory round trip and one CTA barrier.  The
+// round's results then overwrite the raw bytes in place; the pair barrier
+// keeps warp 2c+1's reads ahead of warp 2c's stores (and vice versa).
+template <int R>
+__device__ __forceinline__ void raw_tma_tile_to_regs(const uint4 *smem, uint32_t (&x0)[R], uint32_t (&x1)[R],
+                                                     uint32_t (&x2)[R], uint32_t (&x3)[R]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = warp >> 1, wp = (warp & 1) * 2;
+  const uint32_t *reg = reinterpret_cast<const uint32_t *>(smem) + c * 4096 + wp;
+  uint32_t a[32], b[32];
+#pragma unroll
+  for (int L = 0; L < 32; ++L) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(reg + (32 * L + lane) * 4);
+    a[L] = v.x;
+    b[L] = v.y;
+  }
+  named_sync(1 + c, 64);
+  transpose32(a);
+  transpose32(b);
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    x0[k] = a[k];
+    x1[k] = a[16 + k];
+    x2[k] = b[k];
+    x3[k] = b[16 + k];
+  }
+}
+
 // Bulk-staged packet tile ([position][1024 lanes] of uint16) -> bit-sliced
 // tile in place: warp w owns positions 4w .. 4w+3, two at a time (their 4 KB
 // of rows become their 4 KB of BS blocks), so only warp-level syncs.
@@ -881,6 +912,9 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
   // bit 9: raw row-major output straight from the last round's registers
   // (launch_pass picks it when every tile qualifies, see store_rows_from_regs)
   constexpr bool RREG = (V & 512) && R == 16;
+  // bit 10: TMA-staged raw input tiles go straight into the first round's
+  // registers (raw_tma_tile_to_regs; launch_pass checks the conditions)
+  constexpr bool FUSEIN = (V & 1024) && R == 16;
   constexpr int U4 = Blk<R>::U4;
   // 128-byte aligned: TMA tensor copies land here
   extern __shared__ __align__(128) uint4 smem[];
@@ -967,7 +1001,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
         for (int rb = 0; rb < 4; ++rb)
           tma_load_3d(dst + c * GROUP + rb * 256, &p.tm_merge, 0, c0 + c, g * GROUP + rb * 256, &bar_m);
     }
-    if (RIN && p.in_mode == IO_RAW) {
+    if (RIN && p.in_mode == IO_RAW && !FUSEIN) {
       if (!(PDBG(128))) {
         if (R == 16 && p.raw_tma)
           finish_tile_raw_tma<R>(smem);
@@ -991,7 +1025,9 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
       const bool active = warp < (1 << rr.nw);
       const int q0 = rr.q0w[warp];
       uint32_t a0[R], a1[R], a2[R], a3[R];
-      if (active && !(PDBG(32))) {
+      if (FUSEIN && rd == 0) {
+        if constexpr (FUSEIN) raw_tma_tile_to_regs<R>(smem, a0, a1, a2, a3);
+      } else if (active && !(PDBG(32))) {
         Blk<R>::load(blk(q0), lane, a0);
         Blk<R>::load(blk(q0 | M0), lane, a1);
         if (has1) {
@@ -1285,6 +1321,7 @@ extern template cudaError_t launch_pass_v<16, 0x1100Bu, 40>(const PassParams &, 
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 42>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 56>(const PassParams &, unsigned, size_t, cudaStream_t);
 extern template cudaError_t launch_pass_v<16, 0x1100Bu, 682>(const PassParams &, unsigned, size_t, cudaStream_t);
+extern template cudaError_t launch_pass_v<16, 0x1100Bu, 1177>(const PassParams &, unsigned, size_t, cudaStream_t);
 
 constexpr int GNT = 512;  // gather threads per CTA
 
@@ -1799,6 +1836,15 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
     for (int m = 0; m < p.tpb; ++m) ok = ok && p.gbit[m] == m;
     if (ok) v = 682;
   }
+  // TMA raw input tiles straight into the first round's registers: no
+  // pre-scaling, first round over tile bits (0, 1) with every warp active
+  static const bool no_fusein = std::getenv("LCH_NO_FUSEIN") != nullptr;
+  if (R == 16 && v == 153 && !no_fusein && p.raw_tma && p.tpb == 5 && p.nrounds > 1 && p.npre == 0) {
+    const PassRound &fr = p.rounds[0];
+    bool ok = fr.m0 == 0 && fr.m1 == 1 && fr.nw == 3;
+    for (int w = 0; w < NWARP; ++w) ok = ok && fr.q0w[w] == 4 * w;
+    if (ok) v = 1177;
+  }
   if (std::getenv("LCH_NO_LEAN")) v = 7;
   const size_t smem = pass_smem_bytes(R, p.tpb, p.out_mode == IO_RAW);
   const int64_t total = (int64_t(1) << (p.lgH - p.tpb)) * ngroups;
@@ -1835,6 +1881,7 @@ cudaError_t launch_pass(const PassParams &p, int ngroups, cudaStream_t s) {
       case 40: return launch_pass_v<R, POLY, 40>(p, ctas, smem, s);
       case 42: return launch_pass_v<R, POLY, 42>(p, ctas, smem, s);
       case 682: return launch_pass_v<R, POLY, 682>(p, ctas, smem, s);
+      case 1177: return launch_pass_v<R, POLY, 1177>(p, ctas, smem, s);
       default: return launch_pass_v<R, POLY, 7>(p, ctas, smem, s);
     }
   } else {  // r = 8: the lean and the generic instance only

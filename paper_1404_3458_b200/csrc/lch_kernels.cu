@@ -800,10 +800,13 @@ struct Mul<R, 0u> {
   }
 };
 
+// gdst (optional): the tile's blocks in the BS output buffer -- the scaled
+// blocks then also leave straight from the registers (no later pass over the
+// tile in shared memory to store them).
 template <int R, uint32_t POLY>
 __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *smem,
                                             const uint32_t *tpos, uint32_t base, int TP,
-                                            int64_t trow, const Mul<R, POLY> &mm) {
+                                            int64_t trow, const Mul<R, POLY> &mm, uint4 *gdst = nullptr) {
   constexpr int U4 = Blk<R>::U4;
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
   for (int q = warp; q < TP; q += NWARP) {
@@ -820,6 +823,7 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
       for (int b = 0; b < R; ++b) v[b] = acc[b];
     }
     Blk<R>::store(smem + q * U4, lane, v);
+    if (gdst) Blk<R>::store_g(gdst + size_t(base | tpos[q]) * U4, lane, v);
   }
 }
 
@@ -1167,8 +1171,11 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
       if (!last_reg) __syncthreads();
     }
     if (!reg_path) {
+      // BS output of a scaled tile leaves from the scaling's registers
+      const bool bs_from_scale = POST_OK && p.npost && (!ROUT || p.out_mode == IO_BS) && !(PDBG(5));
       if (POST_OK && p.npost) {
-        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0, mm);
+        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0, mm,
+                             bs_from_scale ? p.bs_out + ((size_t(g) << p.lgH) * U4) : nullptr);
         __syncthreads();
       }
       if (POST_OK && p.gt_out) {
@@ -1192,7 +1199,7 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
         }
       }
       if (!ROUT || p.out_mode == IO_BS) {
-        store_tile_bs<R>(p, bsm, tpos, g, base, TP);
+        if (!bs_from_scale) store_tile_bs<R>(p, bsm, tpos, g, base, TP);
       } else {
         if (R == 16 && p.merge_tma) {
           mbar_wait(&bar_m, phase_m);

@@ -326,9 +326,11 @@ int orc_encode(const orc_ctx *c, uint32_t k, const uint16_t *msg, uint16_t *code
     return rc;
 }
 
-/* rs.py:99-149 */
-int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
-               const uint8_t *erased, uint16_t *out) {
+/* rs.py:99-149.  shared_logs (optional): the locator residues of this erasure
+ * pattern evaluated by the caller -- BatchCodec.decode evaluates the locator
+ * once per shared erasure set (batch.py:126-139), not once per row. */
+static int decode_with_logs(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                            const uint8_t *erased, const uint32_t *shared_logs, uint16_t *out) {
     uint32_t n = c->order;
     if (k < 1 || (k & (k - 1)) || k > n) return ORC_EINVAL;
     if (c->max_h < k) return ORC_EINVAL;
@@ -337,11 +339,12 @@ int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
     if (cnt == 0) { memcpy(out, received, sizeof(uint16_t) * k); return ORC_OK; } /* rs.py:119-120 */
     if (cnt > n - k) return ORC_ETOOMANY;                                          /* rs.py:121-123 */
     if (c->max_h < n) return ORC_EINVAL; /* n-point inverse needs the capacity (transform.py:63-64) */
-    uint32_t *mixed = (uint32_t *)malloc(sizeof(uint32_t) * n);
+    uint32_t *own = shared_logs ? NULL : (uint32_t *)malloc(sizeof(uint32_t) * n);
+    const uint32_t *mixed = shared_logs ? shared_logs : own;
     uint16_t *phi = (uint16_t *)malloc(sizeof(uint16_t) * n);
     uint16_t *dc = (uint16_t *)malloc(sizeof(uint16_t) * n);
-    if (!mixed || !phi || !dc) { free(mixed); free(phi); free(dc); return ORC_ENOMEM; }
-    int rc = orc_locator_logs(c, erased, mixed);
+    if (!mixed || !phi || !dc) { free(own); free(phi); free(dc); return ORC_ENOMEM; }
+    int rc = own ? orc_locator_logs(c, erased, own) : ORC_OK;
     if (!rc) {
         /* rs.py:130-134: phi = received * pi_bar on survivors, 0 on erasures */
         for (uint32_t j = 0; j < n; ++j)
@@ -358,8 +361,13 @@ int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
             }
         }
     }
-    free(mixed); free(phi); free(dc);
+    free(own); free(phi); free(dc);
     return rc;
+}
+
+int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
+               const uint8_t *erased, uint16_t *out) {
+    return decode_with_logs(c, k, received, erased, NULL, out);
 }
 
 /* General k: the reference's decode algorithm (rs.py:125-148)
@@ -367,8 +375,8 @@ int orc_decode(const orc_ctx *c, uint32_t k, const uint16_t *received,
  * erased position.  full[n] = received with each erased j replaced by
  * Phi^d(j) / Pi'(j).  Phi = f * Pi has degree < k + |E| <= n, so the n-point
  * transforms recover f at the erasures for any k. */
-int orc_recover_all(const orc_ctx *c, const uint16_t *received, const uint8_t *erased,
-                    uint16_t *full) {
+static int recover_all_with_logs(const orc_ctx *c, const uint16_t *received, const uint8_t *erased,
+                                 const uint32_t *shared_logs, uint16_t *full) {
     uint32_t n = c->order;
     if (c->max_h < n) return ORC_EINVAL;
     uint32_t cnt = 0;
@@ -376,11 +384,12 @@ int orc_recover_all(const orc_ctx *c, const uint16_t *received, const uint8_t *e
     memcpy(full, received, sizeof(uint16_t) * n);
     if (cnt == 0) return ORC_OK;
     if (cnt == n) return ORC_EINVAL; /* walsh.py:92-93: at least one survivor */
-    uint32_t *mixed = (uint32_t *)malloc(sizeof(uint32_t) * n);
+    uint32_t *own = shared_logs ? NULL : (uint32_t *)malloc(sizeof(uint32_t) * n);
+    const uint32_t *mixed = shared_logs ? shared_logs : own;
     uint16_t *phi = (uint16_t *)malloc(sizeof(uint16_t) * n);
     uint16_t *dc = (uint16_t *)malloc(sizeof(uint16_t) * n);
-    if (!mixed || !phi || !dc) { free(mixed); free(phi); free(dc); return ORC_ENOMEM; }
-    int rc = orc_locator_logs(c, erased, mixed);
+    if (!mixed || !phi || !dc) { free(own); free(phi); free(dc); return ORC_ENOMEM; }
+    int rc = own ? orc_locator_logs(c, erased, own) : ORC_OK;
     if (!rc) {
         for (uint32_t j = 0; j < n; ++j)
             phi[j] = erased[j] ? 0 : (uint16_t)orc_mul(c, received[j], c->exp[mixed[j]]);
@@ -391,8 +400,13 @@ int orc_recover_all(const orc_ctx *c, const uint16_t *received, const uint8_t *e
             for (uint32_t j = 0; j < n; ++j)
                 if (erased[j]) full[j] = (uint16_t)orc_mul(c, dc[j], f_inv(c, c->exp[mixed[j]]));
     }
-    free(mixed); free(phi); free(dc);
+    free(own); free(phi); free(dc);
     return rc;
+}
+
+int orc_recover_all(const orc_ctx *c, const uint16_t *received, const uint8_t *erased,
+                    uint16_t *full) {
+    return recover_all_with_logs(c, received, erased, NULL, full);
 }
 
 /* Systematic encode for any 1 <= k <= n: erasure-decode E = [k, n) from the
@@ -411,8 +425,8 @@ int orc_encode_any(const orc_ctx *c, uint32_t k, const uint16_t *msg, uint16_t *
 }
 
 /* Decode for any 1 <= k <= n: out[k] = positions [0, k) of the recovered word. */
-int orc_decode_any(const orc_ctx *c, uint32_t k, const uint16_t *received,
-                   const uint8_t *erased, uint16_t *out) {
+static int decode_any_with_logs(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                                const uint8_t *erased, const uint32_t *shared_logs, uint16_t *out) {
     uint32_t n = c->order;
     if (k < 1 || k > n) return ORC_EINVAL;
     uint32_t cnt = 0;
@@ -420,10 +434,15 @@ int orc_decode_any(const orc_ctx *c, uint32_t k, const uint16_t *received,
     if (cnt > n - k) return ORC_ETOOMANY;
     uint16_t *full = (uint16_t *)malloc(sizeof(uint16_t) * n);
     if (!full) return ORC_ENOMEM;
-    int rc = orc_recover_all(c, received, erased, full);
+    int rc = recover_all_with_logs(c, received, erased, shared_logs, full);
     if (!rc) memcpy(out, full, sizeof(uint16_t) * k);
     free(full);
     return rc;
+}
+
+int orc_decode_any(const orc_ctx *c, uint32_t k, const uint16_t *received,
+                   const uint8_t *erased, uint16_t *out) {
+    return decode_any_with_logs(c, k, received, erased, NULL, out);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -438,6 +457,7 @@ typedef struct {
     uint16_t *out;
     uint16_t *inout;
     const uint8_t *erased;
+    const uint32_t *shared_logs; /* op 1, shared pattern: locator residues of the batch */
     int64_t begin, end;
     int rc;
 } job_t;
@@ -458,8 +478,10 @@ static void *run_job(void *arg) {
             memcpy(j->out + b * (int64_t)(n - j->k), cw + j->k, sizeof(uint16_t) * (n - j->k));
         } else if (j->op == 1 || j->op == 4) {
             const uint8_t *e = j->erased + (j->shared ? 0 : b * (int64_t)n);
-            j->rc = (j->op == 1 ? orc_decode : orc_decode_any)(c, j->k, j->in + b * (int64_t)n, e,
-                                                               j->out + b * j->k);
+            j->rc = j->op == 1 ? decode_with_logs(c, j->k, j->in + b * (int64_t)n, e, j->shared_logs,
+                                                  j->out + b * j->k)
+                               : decode_any_with_logs(c, j->k, j->in + b * (int64_t)n, e, j->shared_logs,
+                                                      j->out + b * j->k);
         } else {
             uint16_t *a = j->inout + b * (int64_t)j->h;
             j->rc = j->inverse ? orc_inverse(c, a, j->h, j->shift) : orc_forward(c, a, j->h, j->shift);
@@ -490,6 +512,27 @@ static int run_pool(job_t proto, int64_t batch, int nthreads) {
     return rc;
 }
 
+/* Decode drivers.  One shared erasure set: the locator runs once for the
+ * batch, as BatchCodec.decode does (batch.py:126-139); degenerate erasure
+ * counts keep the per-row checks. */
+static int run_decode_pool(job_t p, int64_t batch, int nthreads) {
+    uint32_t *logs = NULL;
+    if (p.shared && batch > 1) {
+        uint32_t n = p.c->order, cnt = 0;
+        for (uint32_t j = 0; j < n; ++j) cnt += p.erased[j] ? 1 : 0;
+        if (cnt > 0 && cnt < n && cnt <= n - p.k && p.k >= 1 && p.k <= n) {
+            logs = (uint32_t *)malloc(sizeof(uint32_t) * n);
+            if (!logs) return ORC_ENOMEM;
+            int rc = orc_locator_logs(p.c, p.erased, logs);
+            if (rc) { free(logs); return rc; }
+            p.shared_logs = logs;
+        }
+    }
+    int rc = run_pool(p, batch, nthreads);
+    free(logs);
+    return rc;
+}
+
 int orc_encode_batch(const orc_ctx *c, uint32_t k, const uint16_t *msg,
                      uint16_t *parity, int64_t batch, int nthreads) {
     job_t p;
@@ -505,7 +548,7 @@ int orc_decode_batch(const orc_ctx *c, uint32_t k, const uint16_t *received,
     memset(&p, 0, sizeof(p));
     p.c = c; p.op = 1; p.k = k; p.in = received; p.out = out;
     p.erased = erased; p.shared = shared_pattern;
-    return run_pool(p, batch, nthreads);
+    return run_decode_pool(p, batch, nthreads);
 }
 
 int orc_encode_any_batch(const orc_ctx *c, uint32_t k, const uint16_t *msg,
@@ -523,7 +566,7 @@ int orc_decode_any_batch(const orc_ctx *c, uint32_t k, const uint16_t *received,
     memset(&p, 0, sizeof(p));
     p.c = c; p.op = 4; p.k = k; p.in = received; p.out = out;
     p.erased = erased; p.shared = shared_pattern;
-    return run_pool(p, batch, nthreads);
+    return run_decode_pool(p, batch, nthreads);
 }
 
 int orc_transform_batch(const orc_ctx *c, uint16_t *a, uint32_t h, uint32_t shift,

@@ -278,15 +278,17 @@ int orc_derivative(const orc_ctx *c, const uint16_t *in, uint16_t *out, uint32_t
     uint16_t *scaled = (uint16_t *)malloc(sizeof(uint16_t) * h);
     if (!scaled) return ORC_ENOMEM;
     for (uint32_t i = 0; i < h; ++i) scaled[i] = (uint16_t)orc_mul(c, in[i], c->b_prod[i]);
-    for (uint32_t j = 0; j < h; ++j) {
-        uint32_t acc = 0;
-        for (int l = 0; l < levels; ++l) {
-            if ((j >> l) & 1) continue;
-            uint32_t src = j + (1u << l);
-            if (src < h) acc ^= scaled[src];
-        }
-        out[j] = acc ? (uint16_t)orc_mul(c, acc, c->b_prod_inv[j]) : 0;
+    /* the gather in the batch codec's order (batch.py:101-106): one pass per
+     * level l over the destinations j with bit l clear, acc[j] ^= scaled[j + 2^l]
+     * (derivative.py:60-70 sums the same terms per j) */
+    memset(out, 0, sizeof(uint16_t) * h);
+    for (int l = 0; l < levels; ++l) {
+        uint32_t step = 1u << l;
+        for (uint32_t blk = 0; blk < h; blk += 2 * step)
+            for (uint32_t j = blk; j < blk + step; ++j) out[j] ^= scaled[j + step];
     }
+    for (uint32_t j = 0; j < h; ++j)
+        out[j] = out[j] ? (uint16_t)orc_mul(c, out[j], c->b_prod_inv[j]) : 0;
     free(scaled);
     return ORC_OK;
 }

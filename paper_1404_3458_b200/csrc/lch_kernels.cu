@@ -1415,6 +1415,13 @@ __global__ void __launch_bounds__(GNT, 2) gather_kernel(const __grid_constant__ 
 #pragma unroll
       for (int b = 0; b < R; ++b) acc[b] ^= x[b];
     }
+    for (int d = 0; d < p.ndirect; ++d) {  // non-tile summed bits: CTA-uniform test
+      if ((pos >> p.dbits[d]) & 1u) continue;
+      uint32_t x[R];
+      ldg(src + size_t(pos | (1u << p.dbits[d])) * U4, w0 + wl, x);
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] ^= x[b];
+    }
     if (p.sb >= 0) {  // the output has the special (top) bit clear
       uint32_t x[R], z[R], cz[R];
       ldg(src + size_t(pos | (1u << p.sb)) * U4, w0 + wl, z);

@@ -144,6 +144,11 @@ struct GatherParams {
   int nnb;
   int nbit[16];
   int lwpc;              // log2 lane-words per CTA (0..5)
+  // summed bits that are NOT tile bits: the partner y[j | 2^dbits[i]] of every
+  // output with that bit clear streams from global memory (the tile then has
+  // fewer positions and more lane-words: longer contiguous runs per position)
+  int ndirect;
+  int dbits[4];
   const uint4 *y;
   const uint4 *t_in;     // may be null
   uint4 *t_out;

@@ -809,6 +809,43 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
                                             int64_t trow, const Mul<R, POLY> &mm, uint4 *gdst = nullptr) {
   constexpr int U4 = Blk<R>::U4;
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
+  if (nops == 1 && TP == 32) {
+    // One scaling of a full tile: every warp reads the tile's 32 factors in
+    // ONE coalesced load (lane l: position l) instead of one dependent global
+    // load per position, and the positions with a nonzero factor -- the only
+    // ones that cost a multiply: the decode's Pi-bar is zero on the erased
+    // positions and Pi'^-1 on the survivors -- are dealt round-robin to the
+    // warps by their rank, so every warp multiplies within one position of
+    // the same count and the barrier behind the phase waits for nobody.
+    const uint32_t fl = uint32_t(__ldg(ops[0].table + trow * ops[0].tab_stride + (base | tpos[lane])));
+    const uint32_t nz = __ballot_sync(0xffffffffu, fl != 0u);
+    const uint32_t lt = (1u << lane) - 1u;
+    // rank of this lane's position among the nonzero ones, then among the zero ones
+    const int rk = fl != 0u ? __popc(nz & lt) : __popc(nz) + __popc(~nz & lt);
+    const bool mine = (rk & (NWARP - 1)) == warp;
+    const uint32_t mine_nz = __ballot_sync(0xffffffffu, mine && fl != 0u);
+    const uint32_t mine_z = __ballot_sync(0xffffffffu, mine && fl == 0u);
+    for (uint32_t m = mine_nz; m; m &= m - 1u) {
+      const int q = __ffs(int(m)) - 1;
+      const uint32_t f = __shfl_sync(0xffffffffu, fl, q);
+      uint32_t v[R], acc[R];
+      Blk<R>::load(smem + q * U4, lane, v);
+#pragma unroll
+      for (int b = 0; b < R; ++b) acc[b] = 0u;
+      mm.acc(acc, v, f);
+      Blk<R>::store(smem + q * U4, lane, acc);
+      if (gdst) Blk<R>::store_g(gdst + size_t(base | tpos[q]) * U4, lane, acc);
+    }
+    for (uint32_t m = mine_z; m; m &= m - 1u) {  // zero factors: the block is zero
+      const int q = __ffs(int(m)) - 1;
+      uint32_t z[R];
+#pragma unroll
+      for (int b = 0; b < R; ++b) z[b] = 0u;
+      Blk<R>::store(smem + q * U4, lane, z);
+      if (gdst) Blk<R>::store_g(gdst + size_t(base | tpos[q]) * U4, lane, z);
+    }
+    return;
+  }
   for (int q = warp; q < TP; q += NWARP) {
     uint32_t v[R];
     Blk<R>::load(smem + q * U4, lane, v);

@@ -800,13 +800,22 @@ struct Mul<R, 0u> {
   }
 };
 
+// The 32 factors of a single scaling over a full tile (lane l: tile position
+// l), requested ahead of the phase so the load's latency hides behind the
+// work in between (the raw tile's transposes, the rounds).
+__device__ __forceinline__ uint32_t scale_factors(const PassOp *ops, const uint32_t *tpos, uint32_t base,
+                                                  int64_t trow) {
+  return uint32_t(__ldg(ops[0].table + trow * ops[0].tab_stride + (base | tpos[threadIdx.x & 31])));
+}
+
 // gdst (optional): the tile's blocks in the BS output buffer -- the scaled
 // blocks then also leave straight from the registers (no later pass over the
 // tile in shared memory to store them).
 template <int R, uint32_t POLY>
 __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *smem,
                                             const uint32_t *tpos, uint32_t base, int TP,
-                                            int64_t trow, const Mul<R, POLY> &mm, uint4 *gdst = nullptr) {
+                                            int64_t trow, const Mul<R, POLY> &mm, uint4 *gdst = nullptr,
+                                            uint32_t fl_early = 0u, bool have_early = false) {
   constexpr int U4 = Blk<R>::U4;
   const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);
   if (nops == 1 && TP == 32) {
@@ -817,7 +826,8 @@ __device__ __forceinline__ void scale_phase(const PassOp *ops, int nops, uint4 *
     // positions and Pi'^-1 on the survivors -- are dealt round-robin to the
     // warps by their rank, so every warp multiplies within one position of
     // the same count and the barrier behind the phase waits for nobody.
-    const uint32_t fl = uint32_t(__ldg(ops[0].table + trow * ops[0].tab_stride + (base | tpos[lane])));
+    // (the caller may have requested the factors earlier: scale_factors)
+    const uint32_t fl = have_early ? fl_early : scale_factors(ops, tpos, base, trow);
     const uint32_t nz = __ballot_sync(0xffffffffu, fl != 0u);
     const uint32_t lt = (1u << lane) - 1u;
     // rank of this lane's position among the nonzero ones, then among the zero ones
@@ -1042,6 +1052,10 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
         for (int rb = 0; rb < 4; ++rb)
           tma_load_3d(dst + c * GROUP + rb * 256, &p.tm_merge, 0, c0 + c, g * GROUP + rb * 256, &bar_m);
     }
+    const int64_t trow = p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0;
+    const bool pre_early = PRE_OK && p.npre == 1 && TP == 32, post_early = POST_OK && p.npost == 1 && TP == 32;
+    uint32_t fl_pre = 0u, fl_post = 0u;
+    if (pre_early) fl_pre = scale_factors(p.pre, tpos, base, trow);
     if (RIN && p.in_mode == IO_RAW && !FUSEIN) {
       if (!(PDBG(128))) {
         if (R == 16 && p.raw_tma)
@@ -1054,9 +1068,10 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
       __syncthreads();
     }
     if (PRE_OK && p.npre) {
-      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0, mm);
+      scale_phase<R, POLY>(p.pre, p.npre, bsm, tpos, base, TP, trow, mm, nullptr, fl_pre, pre_early);
       __syncthreads();
     }
+    if (post_early) fl_post = scale_factors(p.post, tpos, base, trow);
     for (int rd = 0; rd < p.nrounds; ++rd) {
       const PassRound &rr = p.rounds[rd];
       const bool last_reg = reg_path && rd == p.nrounds - 1;
@@ -1211,8 +1226,8 @@ __global__ void __launch_bounds__(NT, LCH_PASS_MINB(V)) pass_kernel(const __grid
       // BS output of a scaled tile leaves from the scaling's registers
       const bool bs_from_scale = POST_OK && p.npost && (!ROUT || p.out_mode == IO_BS) && !(PDBG(5));
       if (POST_OK && p.npost) {
-        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, p.pkt ? (int64_t(g) * GROUP) / p.pkt : 0, mm,
-                             bs_from_scale ? p.bs_out + ((size_t(g) << p.lgH) * U4) : nullptr);
+        scale_phase<R, POLY>(p.post, p.npost, bsm, tpos, base, TP, trow, mm,
+                             bs_from_scale ? p.bs_out + ((size_t(g) << p.lgH) * U4) : nullptr, fl_post, post_early);
         __syncthreads();
       }
       if (POST_OK && p.gt_out) {

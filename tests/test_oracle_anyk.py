@@ -65,3 +65,24 @@ def test_anyk_r16_match_reference_composition(orc16):
         rx = np.where(mask == 1, junk, cw).astype(np.uint16)
         np.testing.assert_array_equal(orc16.decode_any(k, rx, mask), m)
         check_digest(orc16.decode_any(k, junk, mask), c["junk_out"])
+
+
+def test_batch_decode_shared_locator_equals_per_row(orc8, orc16):
+    """A shared erasure set evaluates the locator once per batch
+    (batch.py:126-139); the result must equal the per-row decodes, for the
+    power-of-two codec and the general-k composition, on non-codewords too."""
+    for orc, r, ks in ((orc8, 8, (128, 100)), (orc16, 16, (1 << 15, 49152))):
+        n = 1 << r
+        for k in ks:
+            mask = O.gen_erasures(77 + k, n, n - k, 0, 1)[0]
+            junk = O.gen_symbols(78 + k, r, 0, 3, n)
+            if k & (k - 1) == 0:
+                a = orc.decode_batch(k, junk, mask, 2)
+                b = np.stack([orc.decode(k, junk[i], mask) for i in range(3)])
+                c = orc.decode_batch(k, junk, np.stack([mask] * 3), 2)
+                np.testing.assert_array_equal(a, b)
+                np.testing.assert_array_equal(a, c)
+            a = orc.decode_any_batch(k, junk, mask, 2)
+            b = np.stack([orc.decode_any(k, junk[i], mask) for i in range(3)])
+            np.testing.assert_array_equal(a, b)
+
